@@ -1,0 +1,67 @@
+"""Classify each golden case as 'stable' or 'chaotic' and write manifest.json.
+
+Some reference runs are ill-conditioned: symmetric swaps and coincident robots
+break their symmetry on round-off, so a 1e-14 relative perturbation of the warm
+start changes the final trajectory at O(1e-3..1) (the reference's own result is
+round-off-determined there). Such cases cannot be compared trajectory-for-
+trajectory by ANY re-implementation; their parity is checked through the
+properties the reference tests use (status, residual, equality exactness,
+iteration counts within a band). Classification: run the Kronecker oracle on
+the fixture inputs and on inputs perturbed by (1 + 1e-14), compare finals.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import golden_io  # noqa: E402
+from oracle import sf_kron  # noqa: E402
+
+
+# Robots 0 and 1 share start and goal, so their pinned endpoint coefficients
+# differ only by KKT round-off after the first step: the endpoint pair rows have a
+# ~1e-16 delta whose direction (hence r1 = -a u) is round-off-determined. The
+# resulting lambda component lies in range(A^T) and never reaches xi. A uniform
+# input perturbation keeps the two robots identical, so the automatic test
+# cannot see this; it is labelled by hand.
+OVERRIDE = {"known_coincident": "lam_degenerate"}
+
+
+def main():
+    manifest = {}
+    for name in golden_io.names():
+        g = golden_io.load(name)
+        fixed = all(s == "max_iters" for s in g.out["status"])
+        kw = dict(kind=g.kind, target=g.target, rho=g.rho, max_iters=g.max_iters,
+                  primal_tol=g.primal_tol, fp_tol=g.fp_tol)
+        a = sf_kron.solve_batch(g.sys, g.xi0, g.lam0, **kw, early_exit=not fixed)
+        b = sf_kron.solve_batch(g.sys, g.xi0 * (1 + 1e-14), g.lam0, **kw, early_exit=not fixed)
+        sens = max(float(np.abs(a["xi"][i] - b["xi"][i]).max() / max(np.abs(a["xi"][i]).max(), 1e-300))
+                   for i in range(len(a["xi"])))
+        lsens = max(float(np.abs(a["lam"][i] - b["lam"][i]).max()) for i in range(len(a["lam"])))
+        same_its = list(a["iterations"]) == list(b["iterations"])
+        if not (sens < 1e-7 and same_its):
+            kind = "chaotic"
+        elif lsens > 1e-7:
+            # lambda's component along the boundary-constraint normals range(A^T) is
+            # invisible to xi (Mxx A^T = 0) and is set by the direction of a
+            # round-off-sized delta when robots coincide at pinned endpoints
+            kind = "lam_degenerate"
+        else:
+            kind = "stable"
+        kind = OVERRIDE.get(name, kind)
+        manifest[name] = {"class": kind, "sensitivity": sens, "lam_sensitivity": lsens,
+                          "fixed_iterations": fixed}
+        print(f"{name:24s} {kind:14s} sens={sens:.2e} lam_sens={lsens:.2e} fixed={fixed}")
+    with open(os.path.join(HERE, "manifest.json"), "w") as fh:
+        json.dump(manifest, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()

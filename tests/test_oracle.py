@@ -1,0 +1,80 @@
+"""Pin the CPU oracle (oracle/sf_dense.py, oracle/sf_kron.py) to the reference's
+own outputs stored in tests/golden/*.npz. CPU only.
+
+Cases marked 'chaotic' in tests/golden/manifest.json (symmetric cold-start
+swaps whose symmetry breaks on round-off; see classify.py) are checked through
+the reference tests' properties instead of trajectory equality."""
+
+import numpy as np
+import pytest
+
+import golden_io
+from oracle import sf_dense, sf_kron
+
+# the dense restatement is slow at the C3/C4 shapes: those go through the
+# Kronecker restatement only in the default suite
+DENSE_SKIP = {"c3_inst0_L4", "c4_inst0_L2"}
+MANIFEST = golden_io.manifest()
+
+
+def _run(mod, g, **kw):
+    return mod.solve_batch(g.sys, g.xi0, g.lam0, kind=g.kind, target=g.target, rho=g.rho,
+                           max_iters=g.max_iters, primal_tol=g.primal_tol, fp_tol=g.fp_tol, **kw)
+
+
+def _check(name, out, g, xi_tol):
+    info = MANIFEST[name]
+    if info["class"] == "chaotic":
+        golden_io.assert_properties(out, g)
+        return
+    err = golden_io.compare(out, g.out)
+    assert err["same_iterations"], err
+    assert err["xi_rel"] < xi_tol, err
+    if info["class"] != "lam_degenerate":
+        assert err["lam_abs"] < 1e-7, err
+    assert err["trace_abs"] < 1e-9, err
+    assert err["eq_abs"] < 1e-9, err
+
+
+@pytest.mark.parametrize("name", golden_io.names())
+def test_kron_oracle_matches_reference(name):
+    g = golden_io.load(name)
+    out = _run(sf_kron, g, early_exit=not MANIFEST[name]["fixed_iterations"])
+    # the reference itself drifts ~1e-9 over 500 noise-level iterations (c1)
+    _check(name, out, g, 1e-7)
+
+
+@pytest.mark.parametrize("name", [n for n in golden_io.names() if n not in DENSE_SKIP])
+def test_dense_oracle_matches_reference(name):
+    g = golden_io.load(name)
+    _check(name, _run(sf_dense, g), g, 1e-9)
+
+
+def test_known_answer_overlap_primal():
+    """test_solver.py:246-259: overlapping pair -> primal = 0.1 a sqrt(K+1)."""
+    g = golden_io.load("known_overlap")
+    a = 1.1 * 0.2
+    expect = 0.1 * a * np.sqrt(g.sys.dims.num_steps)
+    assert abs(g.out["trace"][0][0, 0] - expect) < 1e-9
+    out = _run(sf_kron, g, early_exit=False)
+    assert abs(out["trace"][0][0, 0] - expect) < 1e-9
+
+
+def test_kkt_blocks_match_dense_inverse():
+    import scipy.linalg
+    for name, kind in (("obs8_projection", "projection"), ("d3_smoothness", "smoothness"),
+                       ("obs8_free_ends", "projection")):
+        g = golden_io.load(name)
+        d = g.sys.dims
+        sf = sf_kron.KronSF(g.sys, kind, 1.0)
+        F, G, _ = sf_dense.dense_operators(d.n, d.n_obs, g.sys.basis.W)
+        kkt = sf_dense.DenseKkt(F, G, g.sys.A, g.sys.basis.Wdd, d.n, kind, 1.0)
+        Minv = scipy.linalg.lu_solve(kkt.lu, np.eye(kkt.size))
+        nv, n = d.nvar_ax, d.n
+        Mxx = np.kron(np.eye(n), sf.Pxx) + np.kron(np.ones((n, n)) / n, sf.Rxx - sf.Pxx)
+        Mxb = np.kron(np.eye(n), sf.Pxb) + np.kron(np.ones((n, n)) / n, sf.Rxb - sf.Pxb)
+        scale = np.abs(Minv).max()
+        assert np.abs(Minv[:nv, :nv] - Mxx).max() < 1e-12 * scale
+        assert np.abs(Minv[:nv, nv:] - Mxb).max() < 1e-12 * scale
+        M = np.linalg.inv(Minv)
+        assert abs(np.linalg.cond(M) / sf.cond - 1) < 1e-6
