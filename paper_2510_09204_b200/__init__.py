@@ -1,0 +1,16 @@
+"""B200-native batched Safety-Filter (SF) solver of Flow-Opt (arXiv 2510.09204).
+
+Drop-in for `swarmplan.solver.solve_batch` (pkg/src/swarmplan/solver.py:286):
+same signature, same results, computed by a persistent sm_100a kernel
+(`libsfb.so`, C ABI in include/sfb.h)."""
+
+from .errors import (ConfigError, GenerationError, NativeError, SchemaError, SetupError,
+                     ShapeError, UsageError, ValidationError)
+from .problem import (BasisConfig, BasisMatrices, ConstraintSystem, Obstacle, Scenario,
+                      ScenarioFamily, SystemDims, assemble, build_basis, generate,
+                      sample_naive_prior, stack_xi, straight_line_coeffs, xi_from_coeffs)
+from .solver import (BatchResult, DeviceBatch, KktCache, ObjectiveMode, SolverConfig,
+                     SolverResult, SolverState, cold_start, fixed_point_step, solve,
+                     solve_batch, solve_instances, state_from_xi)
+
+__version__ = "0.1.0"

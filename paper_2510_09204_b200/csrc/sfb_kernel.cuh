@@ -1,0 +1,687 @@
+// sfb_kernel.cuh — persistent per-member SF solve kernel for sm_100a.
+//
+// One CTA owns one member (instance x sample) for the whole solve; xi, lambda and
+// every intermediate stay in shared memory / registers across iterations, HBM sees
+// only the warm start, the instance data and the results. One iteration is the map
+// of the reference `_step` (pkg/src/swarmplan/solver.py:211-243), computed through
+// the exact rewrites of DESIGN.md §3 (oracle/sf_kron.py is the FP64 restatement):
+//
+//  A  positions   p_i(k) = sum_c W[k,c] xi_i,c in FP64           (constraints.py:159-163)
+//  B  screening   FP32 packed (FFMA2) r^2 test of every pair / obstacle row of the
+//                 lane's robot against a conservative threshold, one bit per body
+//  B' exact rows  survivors only: FP64 delta, rho = |delta|_scaled, r1 = delta(1 - clip(rho)/rho)
+//                 (constraints.py:166-247), accumulated into g_i(k) (= F^T r1 rows)
+//  B" box rows    r2 = max(p - p_max, 0) - max(p_min - p, 0) (solver.py:166-168)
+//  C  contraction G_i = W^T g_i (= F^T r1 + G^T r2), per-warp partials, fixed-order
+//                 cross-warp sum (deterministic, batch-composition independent)
+//  D  decision    primal = |r1| + |r2| of the input xi, trace, convergence (solver.py:310-337)
+//  E  KKT         lambda+ = lambda - rho G; Delta = 2 lambda+ - lambda + t - Q xi;
+//                 xi+ = xi + (I (x) Pxx + 11^T/n (x) (Rxx - Pxx)) Delta + (same xb) (b - A xi)
+//
+// Thread layout: lanes own robots, a warp owns a k-group (2 consecutive grid steps;
+// n <= 16 packs several k-groups per warp). Pair screening loads the partner's FP32
+// positions with a warp-broadcast LDS.128; the partner's exact FP64 position comes
+// from its owner lane by shuffle (n <= 32) or from FP32 hi/lo pairs in smem (n > 32).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfb {
+
+constexpr int NW = 8;            // warps per CTA
+constexpr int NT = NW * 32;      // threads per CTA
+constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1) step in shared positions
+constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -> never a hit
+constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the reference evaluates it
+
+struct Layout {       // byte offsets into dynamic shared memory
+  int xi, lam, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs, pmax, uni;
+  int uni_bytes, total;
+  int slots;          // G partial slots that fit in the union region per round
+};
+
+struct KParams {
+  int n, m, K1, NB, NKG, LW, RB;
+  int mode, max_iters, early_exit;
+  double rho, primal_tol, fp_tol, d_max, inv_n;
+  float plim;      // FP32 screening valid while max|p| <= plim * (smallest contact axis)
+  Layout L;
+  const double* consts;
+  int B;
+  const int* member_instance;
+  const double* xi0;
+  const double* lam0;
+  const double* target;
+  const double* bvals;
+  const double* box;
+  const double* obs_pos;
+  const double* obs_axes;
+  const double* pair_axes;
+  double* xi;
+  double* lam;
+  double* primal;
+  double* eq_max;
+  int* iterations;
+  int* status;
+  double* trace;
+  unsigned long long* counters;
+};
+
+// plan constant block offsets (doubles)
+struct ConstOff {
+  int W, E, Q, Pxx, Pxb, Dxx, Dxb, total;
+  __host__ __device__ static ConstOff make(int K1, int NXI, int NB) {
+    ConstOff c;
+    c.W = 0;
+    c.E = c.W + K1 * NXI;
+    c.Q = c.E + NB * NXI;
+    c.Pxx = c.Q + NXI * NXI;
+    c.Pxb = c.Pxx + NXI * NXI;
+    c.Dxx = c.Pxb + NXI * NB;
+    c.Dxb = c.Dxx + NXI * NXI;
+    c.total = c.Dxb + NXI * NB;
+    return c;
+  }
+};
+
+__device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
+
+// Exact FP64 residual of one separation row (constraints.py:166-247, trig-free):
+// r1 = delta * (1 - clip(rho, 1, d_max) / rho), coincident rows use alpha = 0, beta = pi/2.
+template <int ND>
+__device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, double inv_b2,
+                                          double ax_a, double ax_b, double d_max,
+                                          double coinc_sign, double (&r)[ND]) {
+  double q = (d[0] * d[0] + d[1] * d[1]) * inv_a2;
+  if (ND == 3) q = fma(d[ND - 1] * d[ND - 1], inv_b2, q);
+  double f;
+  if (q < 1.0) {
+    if (q == 0.0) {
+      r[0] = -ax_a * coinc_sign;
+      r[1] = 0.0 * coinc_sign;
+      if (ND == 3) r[ND - 1] = -ax_b * COS_HALF_PI * coinc_sign;
+      return true;
+    }
+    f = 1.0 - rsqrt(q);
+  } else if (q > d_max * d_max) {
+    f = 1.0 - d_max * rsqrt(q);
+  } else {
+    return false;
+  }
+#pragma unroll
+  for (int a = 0; a < ND; ++a) r[a] = f * d[a];
+  return true;
+}
+
+template <int ND, int NXI, bool BIG>
+__global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
+  constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem[];
+
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = P.n, m = P.m, K1 = P.K1, NB = P.NB, NKG = P.NKG;
+  const int nv = ND * n * NXI;
+  const int inst = P.member_instance[b];
+
+  double* sXi = reinterpret_cast<double*>(smem + P.L.xi);
+  double* sLam = reinterpret_cast<double*>(smem + P.L.lam);
+  double* sW = reinterpret_cast<double*>(smem + P.L.w);      // [NKG][NXI][2]
+  double* sE = reinterpret_cast<double*>(smem + P.L.e);      // [NB][NXI]
+  double* sQ = reinterpret_cast<double*>(smem + P.L.q);      // [NXI][NXI]
+  double* sPxx = reinterpret_cast<double*>(smem + P.L.pxx);
+  double* sPxb = reinterpret_cast<double*>(smem + P.L.pxb);
+  double* sDxx = reinterpret_cast<double*>(smem + P.L.dxx);
+  double* sDxb = reinterpret_cast<double*>(smem + P.L.dxb);
+  double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND][n][NXI]
+  double* sBv = reinterpret_cast<double*>(smem + P.L.bv);    // [ND][n][NB]
+  double* sRed = reinterpret_cast<double*>(smem + P.L.red);  // [NW][4] + misc
+  double* sObsAx = reinterpret_cast<double*>(smem + P.L.obs_ax);   // [m][4] inv_a2 inv_b2 a b
+  float* sObsThr = reinterpret_cast<float*>(smem + P.L.obs_thr);   // [m][2] thr, kappa
+  float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [NKG][m][ND2]
+  float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [NKG][8] (n > 32)
+  unsigned char* uni = smem + P.L.uni;
+  float* sPos = reinterpret_cast<float*>(uni);                      // [NKG][n][ND2] hi
+  float* sLo = sPos + (size_t)NKG * n * ND2;                        // [NKG][n][ND2] lo (BIG)
+  double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots
+  // KKT scratch (aliases the union region after the contraction)
+  double* sD = reinterpret_cast<double*>(uni);                      // [ND][n][NXI]
+  double* sU = sD + nv;                                             // [ND][n][NB]
+  double* sSD = sU + ND * n * NB;                                   // [ND][NXI]
+  double* sSU = sSD + ND * NXI;                                     // [ND][NB]
+
+  const ConstOff co = ConstOff::make(K1, NXI, NB);
+
+  // ------------------------------------------------------------------ setup
+  for (int idx = tid; idx < NKG * NXI * 2; idx += NT) {
+    const int kg = idx / (NXI * 2), rem = idx - kg * NXI * 2, c = rem >> 1, kk = rem & 1;
+    const int k = 2 * kg + kk;
+    sW[idx] = (k < K1) ? P.consts[co.W + k * NXI + c] : 0.0;
+  }
+  for (int idx = tid; idx < NB * NXI; idx += NT) sE[idx] = P.consts[co.E + idx];
+  for (int idx = tid; idx < NXI * NXI; idx += NT) {
+    sQ[idx] = P.consts[co.Q + idx];
+    sPxx[idx] = P.consts[co.Pxx + idx];
+    sDxx[idx] = P.consts[co.Dxx + idx];
+  }
+  for (int idx = tid; idx < NXI * NB; idx += NT) {
+    sPxb[idx] = P.consts[co.Pxb + idx];
+    sDxb[idx] = P.consts[co.Dxb + idx];
+  }
+  {
+    const double* x0 = P.xi0 + (size_t)b * nv;
+    const double* l0 = P.lam0 + (size_t)b * nv;
+    for (int idx = tid; idx < nv; idx += NT) {
+      sXi[idx] = x0[idx];
+      sLam[idx] = l0[idx];
+    }
+    const double* bv = P.bvals + (size_t)inst * ND * n * NB;
+    for (int idx = tid; idx < ND * n * NB; idx += NT) sBv[idx] = bv[idx];
+  }
+  for (int o = tid; o < m; o += NT) {
+    const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
+    const double a = oa[0], bb = oa[2];
+    sObsAx[o * 4 + 0] = 1.0 / (a * a);
+    sObsAx[o * 4 + 1] = 1.0 / (bb * bb);
+    sObsAx[o * 4 + 2] = a;
+    sObsAx[o * 4 + 3] = bb;
+    sObsThr[o * 2 + 0] = (float)(a * a * (1.0 + 2e-3));
+    sObsThr[o * 2 + 1] = (float)((a * a) / (bb * bb));
+  }
+  float obs_absmax = 0.f, obs_axmin = INFINITY;
+  for (int o = tid; o < m; o += NT) {
+    const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
+    obs_axmin = fminf(obs_axmin, (float)(ND == 3 ? fmin(oa[0], oa[2]) : oa[0]));
+  }
+  for (int idx = tid; idx < NKG * m; idx += NT) {
+    const int kg = idx / m, o = idx - kg * m;
+    float* dst = sObs + (size_t)idx * ND2;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+      const double* src = P.obs_pos + (((size_t)inst * ND + a) * m + o) * K1;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = 2 * kg + kk;
+        const float v = (k < K1) ? (float)src[k] : PAD_SMEM;
+        dst[a * 2 + kk] = v;
+        if (k < K1) obs_absmax = fmax_abs(obs_absmax, v);
+      }
+    }
+    if (ND == 3) dst[6] = dst[7] = 0.f;
+  }
+  unsigned* sMisc = reinterpret_cast<unsigned*>(sRed + NW * 4);
+  if (tid == 0) {
+    sMisc[0] = 0u;
+    sMisc[1] = __float_as_uint(INFINITY);
+  }
+  __syncthreads();
+  if (obs_absmax > 0.f) atomicMax(&sMisc[0], __float_as_uint(obs_absmax));
+  if (obs_axmin < INFINITY) atomicMin(&sMisc[1], __float_as_uint(obs_axmin));
+  __syncthreads();
+  obs_absmax = __uint_as_float(sMisc[0]);
+
+  double box_lo[ND], box_hi[ND];
+#pragma unroll
+  for (int a = 0; a < ND; ++a) {
+    box_lo[a] = P.box[((size_t)inst * 2 + 0) * ND + a];
+    box_hi[a] = P.box[((size_t)inst * 2 + 1) * ND + a];
+  }
+  const double ra = P.pair_axes[(size_t)inst * 3 + 0], rb_ax = P.pair_axes[(size_t)inst * 3 + 2];
+  const double r_inv_a2 = 1.0 / (ra * ra), r_inv_b2 = 1.0 / (rb_ax * rb_ax);
+  const float r_thr = (float)(ra * ra * (1.0 + 2e-3));
+  const float r_kap = (float)((ra * ra) / (rb_ax * rb_ax));
+  const double d_max = P.d_max;
+  // FP32 positions carry ~2^-24 |p| error: the screen margin (1e-3 of the contact
+  // distance) covers it while every |p| <= plim; beyond, rows go exact
+  const float plim = P.plim * fminf(__uint_as_float(sMisc[1]),
+                                    (float)(ND == 3 ? fmin(ra, rb_ax) : ra));
+  const double* opos = P.obs_pos + (size_t)inst * ND * m * K1;
+  const double* tgt = P.target ? P.target + (size_t)b * nv : nullptr;
+
+  // lane -> (robot, k-group) mapping
+  int LW, SUB, sub, rbk, wk, nwk;
+  if (BIG) {
+    LW = 32; SUB = 1; sub = 0;
+    rbk = warp % P.RB; wk = warp / P.RB; nwk = NW / P.RB;
+  } else {
+    LW = P.LW; SUB = 32 / LW; sub = lane / LW;
+    rbk = 0; wk = warp; nwk = NW;
+  }
+  const int i = BIG ? rbk * 32 + lane : lane % LW;
+  const bool robot_ok = i < n;
+  const int ic = robot_ok ? i : n - 1;
+  const int NTS = (NKG + SUB - 1) / SUB;
+
+  double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  double eq_max = 0.0;
+  unsigned long long c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
+
+  for (int it = 0;; ++it) {
+    // -------------------------------------------- eq violation of the committed xi
+    double eqp = 0.0;
+    if (it > 0) {
+      for (int idx = tid; idx < ND * n * NB; idx += NT) {
+        const int a = idx / (n * NB), rem = idx - a * n * NB, ii = rem / NB, r = rem - ii * NB;
+        const double* x = sXi + (a * n + ii) * NXI;
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+        eqp = fmax(eqp, fabs(v - sBv[idx]));
+      }
+    }
+
+    // -------------------------------------------- A/B/C per k-group task
+    double Gp[ND][NXI];
+#pragma unroll
+    for (int a = 0; a < ND; ++a)
+#pragma unroll
+      for (int c = 0; c < NXI; ++c) Gp[a][c] = 0.0;
+    double s1 = 0.0, s2 = 0.0;
+
+    for (int ts = wk; ts < NTS; ts += nwk) {
+      const int kg_raw = ts * SUB + sub;
+      const bool kg_ok = kg_raw < NKG;
+      const int kg = kg_ok ? kg_raw : NKG - 1;
+      const bool live = robot_ok && kg_ok;
+      const bool has1 = 2 * kg + 1 < K1;
+      const double2* wk2 = reinterpret_cast<const double2*>(sW + (size_t)kg * NXI * 2);
+
+      // A: exact positions of the lane's robot at the two steps
+      double p[ND][2];
+#pragma unroll
+      for (int a = 0; a < ND; ++a) p[a][0] = p[a][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < NXI; ++c) {
+        const double2 w = wk2[c];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+          const double x = sXi[(a * n + ic) * NXI + c];
+          p[a][0] = fma(w.x, x, p[a][0]);
+          p[a][1] = fma(w.y, x, p[a][1]);
+        }
+      }
+      float own[ND][2];
+      float pabs = 0.f;
+      {
+        float hv[ND2];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+          const float h0 = (float)p[a][0];
+          const float h1 = has1 ? (float)p[a][1] : PAD_SMEM;
+          hv[2 * a] = h0;
+          hv[2 * a + 1] = h1;
+          own[a][0] = live ? h0 : PAD_OWN;
+          own[a][1] = (live && has1) ? h1 : PAD_OWN;
+          if (live) {
+            pabs = fmax_abs(pabs, h0);
+            if (has1) pabs = fmax_abs(pabs, h1);
+          }
+        }
+        if (ND == 3) hv[6] = hv[7] = 0.f;
+        if (live) {
+          float4* dst = reinterpret_cast<float4*>(sPos + ((size_t)kg * n + i) * ND2);
+          dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+          if (BIG) {
+            float lv[ND2];
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+              lv[2 * a] = (float)(p[a][0] - (double)hv[2 * a]);
+              lv[2 * a + 1] = has1 ? (float)(p[a][1] - (double)hv[2 * a + 1]) : 0.f;
+            }
+            if (ND == 3) lv[6] = lv[7] = 0.f;
+            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)kg * n + i) * ND2);
+            dl[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+            if (ND == 3) dl[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
+          }
+        }
+      }
+      pabs = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(pabs)));
+      if (BIG) {
+        if (lane == 0) sPmax[kg * 8 + rbk] = pabs;
+        // every robot block of this k-group must have stored its positions
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + wk), "r"(P.RB * 32) : "memory");
+        for (int r = 0; r < P.RB; ++r) pabs = fmaxf(pabs, sPmax[kg * 8 + r]);
+      } else {
+        __syncwarp();
+      }
+      // conservative FP32 screening is valid while positions stay below plim
+      const bool force = !(fmaxf(pabs, obs_absmax) <= plim);
+      const float2 nx = make_float2(-own[0][0], -own[0][1]);
+      const float2 ny = make_float2(-own[1][0], -own[1][1]);
+      const float2 nz = (ND == 3) ? make_float2(-own[ND - 1][0], -own[ND - 1][1]) : make_float2(0.f, 0.f);
+      const int nsteps = live ? (has1 ? 2 : 1) : 0;
+
+      double g[ND][2];
+#pragma unroll
+      for (int a = 0; a < ND; ++a) g[a][0] = g[a][1] = 0.0;
+
+      // B: robots, in chunks of 32 bodies
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int jc = min(32, n - j0);
+        unsigned mask = 0u;
+        if (!force) {
+          const float2 thr2 = make_float2(-r_thr, -r_thr);
+          const float* base = sPos + ((size_t)kg * n + j0) * ND2;
+#pragma unroll 4
+          for (int j = 0; j < jc; ++j) {
+            const float4 v = *reinterpret_cast<const float4*>(base + (size_t)j * ND2);
+            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+            float2 q = __ffma2_rn(dy, dy, thr2);
+            q = __ffma2_rn(dx, dx, q);
+            if (ND == 3) {
+              const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)j * ND2 + 4);
+              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+              const float2 dzk = __fmul2_rn(dz, make_float2(r_kap, r_kap));
+              q = __ffma2_rn(dzk, dz, q);
+            }
+            const unsigned hit = (__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31;
+            mask |= hit << j;
+          }
+        } else {
+          mask = (jc == 32) ? FULL : ((1u << jc) - 1u);
+        }
+        if (i >= j0 && i < j0 + jc) mask &= ~(1u << (i - j0));
+        if (!live) mask = 0u;
+        c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
+
+        // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)
+        while (__any_sync(FULL, mask != 0u)) {
+          const bool act = mask != 0u;
+          const int jl = act ? __ffs(mask) - 1 : 0;
+          mask &= mask - 1u;
+          const int j = j0 + jl;
+          double pj[ND][2];
+          if (BIG) {
+            const float* hp = sPos + ((size_t)kg * n + (act ? j : 0)) * ND2;
+            const float* lp = sLo + ((size_t)kg * n + (act ? j : 0)) * ND2;
+#pragma unroll
+            for (int a = 0; a < ND; ++a)
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk)
+                pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
+          } else {
+            const int src = sub * LW + jl;
+#pragma unroll
+            for (int a = 0; a < ND; ++a)
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+          }
+          if (act) {
+            const double cs = (i < j) ? 1.0 : -1.0;
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              if (kk < nsteps) {
+                double d[ND], r[ND];
+#pragma unroll
+                for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
+                ++c_exact;
+                if (row_exact<ND>(d, r_inv_a2, r_inv_b2, ra, rb_ax, d_max, cs, r)) {
+                  ++c_active;
+                  double rr = 0.0;
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) {
+                    g[a][kk] += r[a];
+                    rr = fma(r[a], r[a], rr);
+                  }
+                  if (i < j) s1 += rr;
+                }
+              }
+            }
+          }
+        }
+      }
+
+      // B: obstacles, in chunks of 32
+      for (int o0 = 0; o0 < m; o0 += 32) {
+        const int oc = min(32, m - o0);
+        unsigned mask = 0u;
+        if (!force) {
+          const float* base = sObs + ((size_t)kg * m + o0) * ND2;
+#pragma unroll 4
+          for (int o = 0; o < oc; ++o) {
+            const float4 v = *reinterpret_cast<const float4*>(base + (size_t)o * ND2);
+            const float2 tk = *reinterpret_cast<const float2*>(sObsThr + 2 * (o0 + o));
+            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+            float2 q = __ffma2_rn(dy, dy, make_float2(-tk.x, -tk.x));
+            q = __ffma2_rn(dx, dx, q);
+            if (ND == 3) {
+              const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)o * ND2 + 4);
+              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+              const float2 dzk = __fmul2_rn(dz, make_float2(tk.y, tk.y));
+              q = __ffma2_rn(dzk, dz, q);
+            }
+            const unsigned hit = (__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31;
+            mask |= hit << o;
+          }
+        } else {
+          mask = (oc == 32) ? FULL : ((1u << oc) - 1u);
+        }
+        if (!live) mask = 0u;
+        c_screen += (unsigned long long)oc * nsteps;
+        while (mask) {
+          const int o = o0 + __ffs(mask) - 1;
+          mask &= mask - 1u;
+          const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            if (kk < nsteps) {
+              const int k = 2 * kg + kk;
+              double d[ND], r[ND];
+#pragma unroll
+              for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - __ldg(opos + ((size_t)a * m + o) * K1 + k);
+              ++c_exact;
+              if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
+                ++c_active;
+                double rr = 0.0;
+#pragma unroll
+                for (int a = 0; a < ND; ++a) {
+                  g[a][kk] += r[a];
+                  rr = fma(r[a], r[a], rr);
+                }
+                s1 += rr;
+              }
+            }
+          }
+        }
+      }
+
+      // B": workspace box rows (exact, every step)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        if (kk < nsteps) {
+#pragma unroll
+          for (int a = 0; a < ND; ++a) {
+            const double up = p[a][kk] - box_hi[a];
+            const double lo = box_lo[a] - p[a][kk];
+            if (up > 0.0) { g[a][kk] += up; s2 = fma(up, up, s2); }
+            if (lo > 0.0) { g[a][kk] -= lo; s2 = fma(lo, lo, s2); }
+          }
+        }
+      }
+
+      // C: contraction with W^T into the lane's partial G
+      if (__any_sync(FULL, nsteps > 0)) {
+#pragma unroll
+        for (int c = 0; c < NXI; ++c) {
+          const double2 w = wk2[c];
+#pragma unroll
+          for (int a = 0; a < ND; ++a) Gp[a][c] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[a][c]));
+        }
+      }
+      if (BIG) __syncwarp();
+    }
+
+    // -------------------------------------------- reductions
+    if (!BIG) {
+      for (int off = LW; off < 32; off <<= 1) {
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+#pragma unroll
+          for (int c = 0; c < NXI; ++c) Gp[a][c] += __shfl_xor_sync(FULL, Gp[a][c], off);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s1 += __shfl_xor_sync(FULL, s1, off);
+      s2 += __shfl_xor_sync(FULL, s2, off);
+      eqp = fmax(eqp, __shfl_xor_sync(FULL, eqp, off));
+    }
+    if (lane == 0) {
+      sRed[warp * 4 + 0] = s1;
+      sRed[warp * 4 + 1] = s2;
+      sRed[warp * 4 + 2] = eqp;
+    }
+    __syncthreads();   // all positions consumed: the union region is free
+
+    // G partials: slot s of round r holds warp r*slots + s, layout [ND][32][NXI]
+    const int slots = P.L.slots;
+    for (int w0 = 0; w0 < NW; w0 += slots) {
+      if (warp >= w0 && warp < w0 + slots && (BIG ? true : sub == 0) && robot_ok) {
+        double* dst = sSlot + (size_t)(warp - w0) * ND * 32 * NXI;
+        const int li = BIG ? lane : i;
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+#pragma unroll
+          for (int c = 0; c < NXI; ++c) dst[(a * 32 + li) * NXI + c] = Gp[a][c];
+      }
+      __syncthreads();
+      for (int o = tid; o < nv; o += NT) {
+        const int a = o / (n * NXI), rem = o - a * n * NXI, ii = rem / NXI, c = rem - ii * NXI;
+        const int rbi = ii >> 5, li = ii & 31;
+        double acc = (w0 == 0) ? 0.0 : sG[o];
+        for (int w = w0; w < min(NW, w0 + slots); ++w) {
+          if ((BIG ? (w % P.RB) : 0) != rbi) continue;
+          acc += sSlot[(size_t)(w - w0) * ND * 32 * NXI + (a * 32 + li) * NXI + c];
+        }
+        sG[o] = acc;
+      }
+      __syncthreads();
+    }
+
+    // -------------------------------------------- D: residuals, trace, convergence
+    double S1 = 0.0, S2 = 0.0, EQ = 0.0, FP = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      S1 += sRed[w * 4 + 0];
+      S2 += sRed[w * 4 + 1];
+      EQ = fmax(EQ, sRed[w * 4 + 2]);
+      FP += sRed[w * 4 + 3];
+    }
+    const double primal = sqrt(S1) + sqrt(S2);
+    if (it > 0) {
+      last_fp = FP;
+      eq_max = fmax(eq_max, EQ);
+    }
+    ++c_evals;
+    if (tid == 0 && P.trace) {
+      double* tr = P.trace + ((size_t)b * (P.max_iters + 1) + it) * 2;
+      tr[0] = primal;
+      tr[1] = last_fp;
+    }
+    const bool conv_p = P.early_exit && (primal < P.primal_tol) && it >= 1;
+    const bool conv_f = P.early_exit && (last_fp < P.fp_tol);
+    if (conv_p || conv_f || it == P.max_iters) {
+      double* xo = P.xi + (size_t)b * nv;
+      double* lo = P.lam + (size_t)b * nv;
+      for (int idx = tid; idx < nv; idx += NT) {
+        xo[idx] = sXi[idx];
+        lo[idx] = sLam[idx];
+      }
+      if (tid == 0) {
+        P.primal[b] = primal;
+        P.eq_max[b] = eq_max;
+        P.iterations[b] = it;
+        P.status[b] = conv_p ? 1 : (conv_f ? 2 : 0);
+      }
+      break;
+    }
+
+    // -------------------------------------------- E: multiplier update and KKT step
+    double fpp = 0.0;
+    for (int o = tid; o < nv; o += NT) {
+      const int ai = o / NXI, c = o - ai * NXI;
+      const double lo = sLam[o];
+      const double ln = fma(-P.rho, sG[o], lo);
+      double qx;
+      if (P.mode == 0) {
+        qx = sXi[o];
+      } else {
+        qx = 0.0;
+        const double* x = sXi + ai * NXI;
+#pragma unroll
+        for (int c2 = 0; c2 < NXI; ++c2) qx = fma(sQ[c * NXI + c2], x[c2], qx);
+      }
+      const double t = tgt ? tgt[o] : 0.0;
+      sD[o] = 2.0 * ln - lo + t - qx;
+      sLam[o] = ln;
+      const double dl = ln - lo;
+      fpp = fma(dl, dl, fpp);
+    }
+    for (int idx = tid; idx < ND * n * NB; idx += NT) {
+      const int ai = idx / NB, r = idx - ai * NB;
+      const double* x = sXi + ai * NXI;
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+      sU[idx] = sBv[idx] - v;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < ND * (NXI + NB); idx += NT) {
+      const int a = idx / (NXI + NB), cc = idx - a * (NXI + NB);
+      double acc = 0.0;
+      if (cc < NXI) {
+        for (int ii = 0; ii < n; ++ii) acc += sD[(a * n + ii) * NXI + cc];
+        sSD[a * NXI + cc] = acc;
+      } else {
+        const int r = cc - NXI;
+        for (int ii = 0; ii < n; ++ii) acc += sU[(a * n + ii) * NB + r];
+        sSU[a * NB + r] = acc;
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < nv; o += NT) {
+      const int ai = o / NXI, c = o - ai * NXI, a = ai / n;
+      const double* dv = sD + ai * NXI;
+      const double* uv = sU + ai * NB;
+      double acc = 0.0;
+#pragma unroll
+      for (int c2 = 0; c2 < NXI; ++c2) acc = fma(sPxx[c * NXI + c2], dv[c2], acc);
+      for (int r = 0; r < NB; ++r) acc = fma(sPxb[c * NB + r], uv[r], acc);
+      double mean = 0.0;
+#pragma unroll
+      for (int c2 = 0; c2 < NXI; ++c2) mean = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], mean);
+      for (int r = 0; r < NB; ++r) mean = fma(sDxb[c * NB + r], sSU[a * NB + r], mean);
+      const double xo = sXi[o];
+      const double xn = xo + (acc + mean);
+      sXi[o] = xn;
+      const double dx = xn - xo;
+      fpp = fma(dx, dx, fpp);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) fpp += __shfl_xor_sync(FULL, fpp, off);
+    if (lane == 0) sRed[warp * 4 + 3] = fpp;
+    __syncthreads();
+  }
+
+  if (P.counters) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      c_exact += __shfl_xor_sync(FULL, c_exact, off);
+      c_active += __shfl_xor_sync(FULL, c_active, off);
+      c_screen += __shfl_xor_sync(FULL, c_screen, off);
+    }
+    if (lane == 0) {
+      unsigned long long* cb = P.counters + (size_t)b * 4;
+      atomicAdd(cb + 0, c_exact);
+      atomicAdd(cb + 1, c_active);
+      atomicAdd(cb + 2, c_screen);
+      if (warp == 0) atomicAdd(cb + 3, c_evals);
+    }
+  }
+}
+
+}  // namespace sfb
