@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — SF-solved instances/s of the B200 batched Safety-Filter solver.
+
+Workload (BASELINE.json configs[2], "C3"): 32 robots, 20 circular obstacles in a
+[-2, 2]^2 box, T = K+1 = 100 grid steps, n_basis = 11; per GPU a batch of 64
+instances x 8 samples = 512 members; fixed L = 500 iterations (501 map evaluations
+per member, the paper's Fig. 6b protocol). Inputs are synthetic:
+scenarios from the reference generator (restated in problem.py), samples from the
+naive prior (stand-in for flow samples), warm start (target, lambda = 0).
+
+One step = one SF solve of the rank's whole batch. `value` is timed on the device
+(CUDA events around the kernel, inputs resident in HBM, L2 flushed between steps);
+`e2e` goes through the public API `solve_instances` with host inputs (H2D + D2H
+inside the timed region). `--impl reference` times the reference algorithm
+(oracle/sf_dense.py, the faithful dense restatement) on the host cores instead.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SF-solved instances/sec (32 robots, T=100) at 1/2/4/8 B200; p50 SF latency"
+WL = dict(name="C3", n=32, m=20, h=2.0, K1=100, n_basis=11, duration=5.0, instances=64,
+          samples=8, L=500, robot_radius=0.1, obstacle_radius=0.15)
+NOMINAL = {"fp32_ffma2_tflops": 74.4, "fp64_dfma_tflops": 37.2, "mufu_rsq_tops": 4.65}
+
+
+# ------------------------------------------------------------------ workload
+def make_workload(rank: int, wl=WL):
+    from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble, build_basis,
+                                               generate, sample_naive_prior, stack_xi)
+    from paper_2510_09204_b200.solver import to_member_major
+    basis = build_basis(BasisConfig(wl["n_basis"], wl["K1"], wl["duration"]))
+    fam = ScenarioFamily("random_box", robot_radius=wl["robot_radius"], box=(-wl["h"], wl["h"]),
+                         n_obstacles=wl["m"], obstacle_radius=wl["obstacle_radius"])
+    systems, xs = [], []
+    for i in range(wl["instances"]):
+        seed = 3000 + rank * 100000 + i
+        scn = generate(fam, wl["n"], 2, seed=seed, horizon=basis.config)
+        systems.append(assemble(scn, basis))
+        xs.append(stack_xi(sample_naive_prior(scn, basis, wl["samples"], seed=seed)))
+    xi = to_member_major(np.concatenate(xs, axis=-1), wl["n"], wl["n_basis"])
+    mi = np.repeat(np.arange(wl["instances"]), wl["samples"]).astype(np.int32)
+    return systems, xi, mi
+
+
+# ------------------------------------------------------------------ roofline model
+def algorithmic_ops(n, m, K1, nxi, nd, nb, active_rows, evals):
+    """SURVEY.md §8(d) screened formulation, summed over `evals` member-iterations with
+    `active_rows` active separation rows in total (pairs counted once)."""
+    P = n * (n - 1) // 2
+    R = (P + n * m) * K1
+    nv = n * nxi
+    kkt = nd * (2 * n * nxi * (nxi + 6) + 2 * n * (nxi + 6) + 2 * nxi * (nxi + 6) + n * nxi) \
+        + 2 * nd * nb * n * nxi
+    o32 = evals * (2 * nd * n * K1 * nxi + 6 * R + 8 * nd * n * K1) + 11 * active_rows
+    o64 = evals * (2 * nd * n * K1 * nxi + kkt + 10 * nd * nv) + 4 * active_rows
+    return float(o32), float(o64)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "profiles", "peaks_b200.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return p, "measured (profiles/peaks_b200.json, tools/measure_peaks.py)"
+    return dict(NOMINAL), "nominal (148 SMs x 1.965 GHz); peaks not measured"
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.th.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU legs
+_CPU_STATE = {}
+
+
+def _cpu_init(wl, L_cpu):
+    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    _CPU_STATE["wl"] = wl
+    _CPU_STATE["L"] = L_cpu
+
+
+def _cpu_task(i):
+    """One instance (all S samples) through the faithful dense restatement of the
+    reference solve_batch (oracle/sf_dense.py); returns (setup_s, solve_s, evals)."""
+    from oracle import sf_dense
+    from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble, build_basis,
+                                               generate, sample_naive_prior, stack_xi)
+    wl, L = _CPU_STATE["wl"], _CPU_STATE["L"]
+    basis = build_basis(BasisConfig(wl["n_basis"], wl["K1"], wl["duration"]))
+    fam = ScenarioFamily("random_box", robot_radius=wl["robot_radius"], box=(-wl["h"], wl["h"]),
+                         n_obstacles=wl["m"], obstacle_radius=wl["obstacle_radius"])
+    seed = 3000 + i
+    scn = generate(fam, wl["n"], 2, seed=seed, horizon=basis.config)
+    sys_ = assemble(scn, basis)
+    xi = stack_xi(sample_naive_prior(scn, basis, wl["samples"], seed=seed))
+    t0 = time.perf_counter()
+    sf = sf_dense.DenseSF(sys_, "projection", 1.0)
+    t1 = time.perf_counter()
+    sf_dense.solve_batch(sys_, xi, np.zeros_like(xi), kind="projection", target=xi, max_iters=L,
+                         primal_tol=1e-300, fp_tol=1e-300, sf=sf)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, wl["samples"] * (L + 1)
+
+
+def cpu_workers():
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available
+        n = min(n, max(1, int(mem // (3 << 30))))   # dense F + temporaries ~2-3 GB per process at C3
+    except Exception:
+        pass
+    return max(1, min(n, 64))
+
+
+class CpuReference:
+    """Pool of W processes, one instance per process and step."""
+
+    def __init__(self, L_cpu=2, workers=None):
+        self.W = workers or cpu_workers()
+        self.L = L_cpu
+        ctx = mp.get_context("fork")
+        self.pool = ctx.Pool(self.W, initializer=_cpu_init, initargs=(WL, L_cpu))
+
+    def step(self):
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_task, range(self.W))
+        wall = time.perf_counter() - t0
+        setup = sum(r[0] for r in res) / len(res)
+        solve = max(r[1] for r in res)
+        evals = sum(r[2] for r in res)
+        # instances/s at L = WL["L"]: member-evaluations per second / evaluations per instance
+        per_inst = WL["samples"] * (WL["L"] + 1)
+        return {"inst_per_s": evals / solve / per_inst, "wall": wall, "setup_s": setup,
+                "solve_s": solve, "evals": evals}
+
+    def close(self):
+        self.pool.terminate()
+
+    def describe(self):
+        return {"cores": self.W, "kind": "port",
+                "sample": (f"{self.W} instances in parallel (1 per process, 1 thread each), "
+                           f"{WL['samples']} samples x {self.L + 1} map evaluations each through "
+                           f"oracle/sf_dense.py (dense-F restatement of solver.py:286-355), "
+                           f"extrapolated to L={WL['L']} (per-iteration cost is constant); "
+                           f"setup (F, F^T F, LU) excluded like the GPU plan")}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ref = CpuReference(L_cpu=args.cpu_iters)
+    for _ in range(args.warmup):
+        ref.step()
+    vals = [ref.step() for _ in range(args.steps)]
+    ref.close()
+    v = statistics.mean(r["inst_per_s"] for r in vals)
+    ms = statistics.mean(r["solve_s"] for r in vals) * 1e3
+    desc = ref.describe()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.gpus),
+        "cpu_baseline": {"value": v, "unit": "instances/s", **desc},
+        "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s_per_instance": statistics.mean(r["setup_s"] for r in vals),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(n_gpus):
+    return {"workload": "C3: 32 robots, 20 obstacles, box [-2,2]^2, T=100, n_basis=11, "
+                        "64 instances x 8 samples per GPU, L=500 fixed iterations",
+            "robots": WL["n"], "obstacles": WL["m"], "T": WL["K1"], "instances_per_gpu": WL["instances"],
+            "samples": WL["samples"], "iterations": WL["L"], "parallelism": f"instance-shard x{n_gpus}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2510_09204_b200 import solver
+    from paper_2510_09204_b200.parallel import gather_results
+
+    systems, xi, mi = make_workload(rank)
+    cfg = solver.SolverConfig(max_iters=WL["L"])
+    B = xi.shape[0]
+
+    # ---- device-resident batch (kernel timing)
+    batch = solver.DeviceBatch(systems, xi, None, xi, cfg=cfg, member_instance=mi, early_exit=False,
+                               trace=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        batch.launch()
+    torch.cuda.synchronize()
+    # counters from one extra (untimed) solve: active rows for the roofline model
+    cbatch = solver.DeviceBatch(systems, xi, None, xi, cfg=cfg, member_instance=mi, early_exit=False,
+                                trace=False, counters=True)
+    cbatch.launch()
+    counters = cbatch.out_counters.cpu().numpy()
+    del cbatch
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t_wall = time.perf_counter()
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            starts[s].record(stream)
+            batch.launch(stream)
+            if world > 1:
+                gather_results(batch, dst=0)
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    t_dev = sum(ms) / 1e3
+    if world > 1:
+        t = torch.tensor([t_dev], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_dev = float(t.item())
+        dist.barrier()
+    inst_total = WL["instances"] * world * args.steps
+    value = inst_total / t_dev
+
+    # ---- roofline of the kernel
+    peaks, peak_src = load_peaks()
+    evals = int(counters[:, 3].sum())
+    active = int(counters[:, 1].sum())
+    o32, o64 = algorithmic_ops(WL["n"], WL["m"], WL["K1"], WL["n_basis"], 2, 6, active, evals)
+    t_launch = t_dev / args.steps if world == 1 else statistics.mean(ms) / 1e3
+    a32, a64 = o32 / t_launch / 1e12, o64 / t_launch / 1e12
+    p32, p64 = peaks["fp32_ffma2_tflops"], peaks["fp64_dfma_tflops"]
+    bound32 = o32 / p32 >= o64 / p64
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    roof = {"bound": "fp32" if bound32 else "fp64", "achieved": a32 if bound32 else a64,
+            "peak": p32 if bound32 else p64, "unit": "TFLOP/s",
+            "frac": (a32 / p32) if bound32 else (a64 / p64), "traffic": traffic,
+            "peak_source": peak_src,
+            "model": ("SURVEY.md §8(d) screened formulation per member-iteration: FP32 = 2*n_d*n*K1*n_xi "
+                      "+ 6*R + 8*n_d*n*K1 + 11*A, FP64 = 2*n_d*n*K1*n_xi + KKT_kron + 10*n_d*nv + 4*A; "
+                      "R = (n(n-1)/2 + n*m)*K1 rows, A = active rows counted by the kernel"),
+            "fp32_tflop_per_launch": o32 / 1e12, "fp64_tflop_per_launch": o64 / 1e12,
+            "fp64_frac": a64 / p64, "active_rows_per_eval": active / max(evals, 1),
+            "exact_rows_per_eval": float(counters[:, 0].sum()) / max(evals, 1)}
+
+    # ---- end to end through the public API (host arrays, pinned)
+    xi_pin = torch.from_numpy(xi).pin_memory()
+    e2e_times = []
+    h2d = d2h = 0
+    for s in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = solver.solve_instances(systems, xi_pin, None, xi_pin, cfg=cfg, member_instance=mi,
+                                     fixed_iterations=True, trace=True)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            e2e_times.append(dt)
+    h2d = res.extra.get("h2d_bytes", 0)
+    d2h = res.extra.get("d2h_bytes", 0)
+    t_e2e = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = WL["instances"] * world * args.steps / t_e2e
+
+    # ---- p50 latency of one instance (8 samples, L=500) host to host
+    lat = None
+    if rank == 0 and args.latency > 0:
+        lat_t = []
+        for k in range(args.latency + 2):
+            i = k % WL["instances"]
+            sel = slice(i * WL["samples"], (i + 1) * WL["samples"])
+            t0 = time.perf_counter()
+            solver.solve_instances([systems[i]], xi[sel], None, xi[sel], cfg=cfg,
+                                   fixed_iterations=True, trace=True)
+            if k >= 2:
+                lat_t.append(time.perf_counter() - t0)
+        lat = {"p50_ms": 1e3 * statistics.median(lat_t), "n": len(lat_t),
+               "what": "one instance (8 samples, L=500) via solve_instances, host arrays in/out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ref = CpuReference(L_cpu=args.cpu_iters)
+        r = ref.step()
+        ref.close()
+        cpu = {"value": r["inst_per_s"], "unit": "instances/s", **ref.describe(),
+               "setup_s_per_instance": r["setup_s"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference random_box generator + naive-prior samples)",
+            "config": config_dict(world),
+            "e2e": {"value": e2e_value, "unit": "instances/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * world,
+            "roofline": roof, "cpu_baseline": cpu, "latency": lat,
+            "clocks": clk.summary(), "wall_s_timed": t_wall,
+            "members_per_gpu": B, "map_evaluations_per_member": WL["L"] + 1,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-iters", type=int, default=2, help="fixed iterations per CPU sample")
+    ap.add_argument("--latency", type=int, default=30, help="instances for the p50 latency (0: skip)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -71,6 +71,9 @@ void sfb_plan_destroy(sfb_plan* plan);
 /* cond(M) of the full KKT matrix, as np.linalg.cond would report it */
 double sfb_plan_cond(const sfb_plan* plan);
 
+/* sfb_batch.flags */
+#define SFB_BATCH_STATIC_OBSTACLES 1  /* caller guarantees obs_pos is constant over the steps */
+
 typedef struct sfb_batch {
   int32_t n_members;               /* B                                                   */
   int32_t n_instances;             /* I (distinct constraint systems)                     */
@@ -83,6 +86,7 @@ typedef struct sfb_batch {
   const double* obs_pos;           /* [I][n_d][n_obs][num_steps] ConstraintSystem.obs_pos */
   const double* obs_axes;          /* [I][n_obs][3]  ConstraintSystem.obs_axes            */
   const double* pair_axes;         /* [I][3]         ConstraintSystem.pair_axes           */
+  int32_t flags;                   /* SFB_BATCH_* hints                                   */
 } sfb_batch;
 
 typedef struct sfb_config {

@@ -10,7 +10,7 @@ import os
 from .errors import NativeError, SetupError, ShapeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfb.so")
+LIB_PATH = os.environ.get("SFB_LIB", os.path.join(HERE, "libsfb.so"))
 
 SFB_OK, SFB_EINVAL, SFB_ESETUP, SFB_ECUDA, SFB_ENOMEM = 0, 1, 2, 3, 4
 MODE = {"projection": 0, "smoothness": 1}
@@ -30,7 +30,10 @@ class Batch(ctypes.Structure):
                 ("lam0", ctypes.c_void_p), ("target", ctypes.c_void_p),
                 ("bvals", ctypes.c_void_p), ("box", ctypes.c_void_p),
                 ("obs_pos", ctypes.c_void_p), ("obs_axes", ctypes.c_void_p),
-                ("pair_axes", ctypes.c_void_p)]
+                ("pair_axes", ctypes.c_void_p), ("flags", ctypes.c_int32)]
+
+
+BATCH_STATIC_OBSTACLES = 1
 
 
 class Config(ctypes.Structure):

@@ -35,13 +35,13 @@ constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -
 constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the reference evaluates it
 
 struct Layout {       // byte offsets into dynamic shared memory
-  int xi, lam, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs, pmax, uni;
+  int xi, lam, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs, pmax, uni;
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
 };
 
 struct KParams {
-  int n, m, K1, NB, NKG, LW, RB;
+  int n, m, MP, K1, NB, NKG, RB, obs_static;
   int mode, max_iters, early_exit;
   double rho, primal_tol, fp_tol, d_max, inv_n;
   float plim;      // FP32 screening valid while max|p| <= plim * (smallest contact axis)
@@ -113,15 +113,19 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
   return true;
 }
 
-template <int ND, int NXI, bool BIG>
-__global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
+// NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
+template <int ND, int NXI, int NJ, bool BIG>
+#ifndef SFB_MINB
+#define SFB_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = P.n, m = P.m, K1 = P.K1, NB = P.NB, NKG = P.NKG;
+  const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
   const int nv = ND * n * NXI;
   const int inst = P.member_instance[b];
 
@@ -137,13 +141,17 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
   double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND][n][NXI]
   double* sBv = reinterpret_cast<double*>(smem + P.L.bv);    // [ND][n][NB]
   double* sRed = reinterpret_cast<double*>(smem + P.L.red);  // [NW][4] + misc
-  double* sObsAx = reinterpret_cast<double*>(smem + P.L.obs_ax);   // [m][4] inv_a2 inv_b2 a b
-  float* sObsThr = reinterpret_cast<float*>(smem + P.L.obs_thr);   // [m][2] thr, kappa
-  float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [NKG][m][ND2]
+  double* sObsAx = reinterpret_cast<double*>(smem + P.L.obs_ax);   // [MP][4] inv_a2 inv_b2 a b
+  float* sObsThr = reinterpret_cast<float*>(smem + P.L.obs_thr);   // [2][MP] thr, kappa
+  double* sObsC = reinterpret_cast<double*>(smem + P.L.obs_c);     // [MP][ND] exact centers (static)
+  float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [static ? 1 : NKG][MP][ND2]
   float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [NKG][8] (n > 32)
   unsigned char* uni = smem + P.L.uni;
-  float* sPos = reinterpret_cast<float*>(uni);                      // [NKG][n][ND2] hi
-  float* sLo = sPos + (size_t)NKG * n * ND2;                        // [NKG][n][ND2] lo (BIG)
+  constexpr int dummy_nj = NJ;
+  (void)dummy_nj;
+  const int NROW = BIG ? n : NJ;                                    // bodies per k-group row
+  float* sPos = reinterpret_cast<float*>(uni);                      // [NKG][NROW][ND2] hi
+  float* sLo = sPos + (size_t)NKG * NROW * ND2;                     // [NKG][NROW][ND2] lo (BIG)
   double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots
   // KKT scratch (aliases the union region after the contraction)
   double* sD = reinterpret_cast<double*>(uni);                      // [ND][n][NXI]
@@ -179,33 +187,44 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
     const double* bv = P.bvals + (size_t)inst * ND * n * NB;
     for (int idx = tid; idx < ND * n * NB; idx += NT) sBv[idx] = bv[idx];
   }
-  for (int o = tid; o < m; o += NT) {
-    const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
-    const double a = oa[0], bb = oa[2];
-    sObsAx[o * 4 + 0] = 1.0 / (a * a);
-    sObsAx[o * 4 + 1] = 1.0 / (bb * bb);
-    sObsAx[o * 4 + 2] = a;
-    sObsAx[o * 4 + 3] = bb;
-    sObsThr[o * 2 + 0] = (float)(a * a * (1.0 + 2e-3));
-    sObsThr[o * 2 + 1] = (float)((a * a) / (bb * bb));
+  // obstacles, padded to MP (multiple of 4) with far-away dummies that never screen in
+  for (int o = tid; o < MP; o += NT) {
+    if (o < m) {
+      const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
+      const double a = oa[0], bb = oa[2];
+      sObsAx[o * 4 + 0] = 1.0 / (a * a);
+      sObsAx[o * 4 + 1] = 1.0 / (bb * bb);
+      sObsAx[o * 4 + 2] = a;
+      sObsAx[o * 4 + 3] = bb;
+      sObsThr[o] = (float)(a * a * (1.0 + 2e-3));
+      sObsThr[MP + o] = (float)((a * a) / (bb * bb));
+#pragma unroll
+      for (int a2 = 0; a2 < ND; ++a2) sObsC[o * ND + a2] = P.obs_pos[(((size_t)inst * ND + a2) * m + o) * K1];
+    } else {
+      sObsThr[o] = 0.f;
+      sObsThr[MP + o] = 0.f;
+    }
   }
   float obs_absmax = 0.f, obs_axmin = INFINITY;
   for (int o = tid; o < m; o += NT) {
     const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
     obs_axmin = fminf(obs_axmin, (float)(ND == 3 ? fmin(oa[0], oa[2]) : oa[0]));
   }
-  for (int idx = tid; idx < NKG * m; idx += NT) {
-    const int kg = idx / m, o = idx - kg * m;
+  const int NKGO = P.obs_static ? 1 : NKG;
+  for (int idx = tid; idx < NKGO * MP; idx += NT) {
+    const int kg = idx / MP, o = idx - kg * MP;
     float* dst = sObs + (size_t)idx * ND2;
 #pragma unroll
     for (int a = 0; a < ND; ++a) {
-      const double* src = P.obs_pos + (((size_t)inst * ND + a) * m + o) * K1;
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        const int k = 2 * kg + kk;
-        const float v = (k < K1) ? (float)src[k] : PAD_SMEM;
+        const int k = P.obs_static ? 0 : 2 * kg + kk;
+        float v = PAD_SMEM;
+        if (o < m && k < K1) {
+          v = (float)P.obs_pos[(((size_t)inst * ND + a) * m + o) * K1 + k];
+          obs_absmax = fmax_abs(obs_absmax, v);
+        }
         dst[a * 2 + kk] = v;
-        if (k < K1) obs_absmax = fmax_abs(obs_absmax, v);
       }
     }
     if (ND == 3) dst[6] = dst[7] = 0.f;
@@ -240,12 +259,13 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
   const double* tgt = P.target ? P.target + (size_t)b * nv : nullptr;
 
   // lane -> (robot, k-group) mapping
-  int LW, SUB, sub, rbk, wk, nwk;
+  constexpr int LW = BIG ? 32 : NJ, SUB = 32 / LW;
+  int sub, rbk, wk, nwk;
   if (BIG) {
-    LW = 32; SUB = 1; sub = 0;
+    sub = 0;
     rbk = warp % P.RB; wk = warp / P.RB; nwk = NW / P.RB;
   } else {
-    LW = P.LW; SUB = 32 / LW; sub = lane / LW;
+    sub = lane / LW;
     rbk = 0; wk = warp; nwk = NW;
   }
   const int i = BIG ? rbk * 32 + lane : lane % LW;
@@ -308,19 +328,16 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
           const float h0 = (float)p[a][0];
-          const float h1 = has1 ? (float)p[a][1] : PAD_SMEM;
-          hv[2 * a] = h0;
-          hv[2 * a + 1] = h1;
+          const float h1 = (float)p[a][1];
+          pabs = fmaxf(pabs, fmaxf(fabsf(h0), fabsf(h1)));
+          hv[2 * a] = robot_ok ? h0 : PAD_SMEM;
+          hv[2 * a + 1] = (robot_ok && has1) ? h1 : PAD_SMEM;
           own[a][0] = live ? h0 : PAD_OWN;
           own[a][1] = (live && has1) ? h1 : PAD_OWN;
-          if (live) {
-            pabs = fmax_abs(pabs, h0);
-            if (has1) pabs = fmax_abs(pabs, h1);
-          }
         }
         if (ND == 3) hv[6] = hv[7] = 0.f;
-        if (live) {
-          float4* dst = reinterpret_cast<float4*>(sPos + ((size_t)kg * n + i) * ND2);
+        if (kg_ok && (!BIG || robot_ok)) {
+          float4* dst = reinterpret_cast<float4*>(sPos + ((size_t)kg * NROW + i) * ND2);
           dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
           if (BIG) {
@@ -331,7 +348,7 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
               lv[2 * a + 1] = has1 ? (float)(p[a][1] - (double)hv[2 * a + 1]) : 0.f;
             }
             if (ND == 3) lv[6] = lv[7] = 0.f;
-            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)kg * n + i) * ND2);
+            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)kg * NROW + i) * ND2);
             dl[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
             if (ND == 3) dl[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
           }
@@ -357,35 +374,50 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
 #pragma unroll
       for (int a = 0; a < ND; ++a) g[a][0] = g[a][1] = 0.0;
 
-      // B: robots, in chunks of 32 bodies
-      for (int j0 = 0; j0 < n; j0 += 32) {
-        const int jc = min(32, n - j0);
+      // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
+      for (int j0 = 0; j0 < (BIG ? n : 1); j0 += 32) {
+        const int jc = BIG ? min(32, n - j0) : n;
         unsigned mask = 0u;
         if (!force) {
           const float2 thr2 = make_float2(-r_thr, -r_thr);
-          const float* base = sPos + ((size_t)kg * n + j0) * ND2;
+          const float* base = sPos + ((size_t)kg * NROW + j0) * ND2;
+          if (BIG) {
 #pragma unroll 4
-          for (int j = 0; j < jc; ++j) {
-            const float4 v = *reinterpret_cast<const float4*>(base + (size_t)j * ND2);
-            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-            float2 q = __ffma2_rn(dy, dy, thr2);
-            q = __ffma2_rn(dx, dx, q);
-            if (ND == 3) {
-              const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)j * ND2 + 4);
-              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-              const float2 dzk = __fmul2_rn(dz, make_float2(r_kap, r_kap));
-              q = __ffma2_rn(dzk, dz, q);
+            for (int j = 0; j < jc; ++j) {
+              const float4 v = *reinterpret_cast<const float4*>(base + (size_t)j * ND2);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+              float2 q = __ffma2_rn(dy, dy, thr2);
+              q = __ffma2_rn(dx, dx, q);
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)j * ND2 + 4);
+                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
+              }
+              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << j;
             }
-            const unsigned hit = (__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31;
-            mask |= hit << j;
+          } else {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              const float4 v = *reinterpret_cast<const float4*>(base + j * ND2);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+              float2 q = __ffma2_rn(dy, dy, thr2);
+              q = __ffma2_rn(dx, dx, q);
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(base + j * ND2 + 4);
+                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
+              }
+              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << j;
+            }
           }
         } else {
-          mask = (jc == 32) ? FULL : ((1u << jc) - 1u);
+          mask = (jc >= 32) ? FULL : ((1u << jc) - 1u);
         }
         if (i >= j0 && i < j0 + jc) mask &= ~(1u << (i - j0));
         if (!live) mask = 0u;
-        c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
+        if (P.counters) c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
 
         // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)
         while (__any_sync(FULL, mask != 0u)) {
@@ -395,8 +427,8 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
           const int j = j0 + jl;
           double pj[ND][2];
           if (BIG) {
-            const float* hp = sPos + ((size_t)kg * n + (act ? j : 0)) * ND2;
-            const float* lp = sLo + ((size_t)kg * n + (act ? j : 0)) * ND2;
+            const float* hp = sPos + ((size_t)kg * NROW + (act ? j : 0)) * ND2;
+            const float* lp = sLo + ((size_t)kg * NROW + (act ? j : 0)) * ND2;
 #pragma unroll
             for (int a = 0; a < ND; ++a)
 #pragma unroll
@@ -419,7 +451,7 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
                 for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
                 ++c_exact;
                 if (row_exact<ND>(d, r_inv_a2, r_inv_b2, ra, rb_ax, d_max, cs, r)) {
-                  ++c_active;
+                  if (i < j) ++c_active;   // each pair row once, like the reference's F rows
                   double rr = 0.0;
 #pragma unroll
                   for (int a = 0; a < ND; ++a) {
@@ -434,34 +466,42 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
         }
       }
 
-      // B: obstacles, in chunks of 32
-      for (int o0 = 0; o0 < m; o0 += 32) {
-        const int oc = min(32, m - o0);
+      // B: obstacles (padded to MP), in chunks of 32
+      const float* obase = sObs + (P.obs_static ? 0 : (size_t)kg * MP * ND2);
+      for (int o0 = 0; o0 < MP; o0 += 32) {
+        const int oc = min(32, MP - o0);
         unsigned mask = 0u;
         if (!force) {
-          const float* base = sObs + ((size_t)kg * m + o0) * ND2;
-#pragma unroll 4
-          for (int o = 0; o < oc; ++o) {
-            const float4 v = *reinterpret_cast<const float4*>(base + (size_t)o * ND2);
-            const float2 tk = *reinterpret_cast<const float2*>(sObsThr + 2 * (o0 + o));
-            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-            float2 q = __ffma2_rn(dy, dy, make_float2(-tk.x, -tk.x));
-            q = __ffma2_rn(dx, dx, q);
-            if (ND == 3) {
-              const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)o * ND2 + 4);
-              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-              const float2 dzk = __fmul2_rn(dz, make_float2(tk.y, tk.y));
-              q = __ffma2_rn(dzk, dz, q);
+#pragma unroll 2
+          for (int o4 = 0; o4 < oc; o4 += 4) {
+            const float4 th = *reinterpret_cast<const float4*>(sObsThr + o0 + o4);
+            const float thv[4] = {th.x, th.y, th.z, th.w};
+            float4 kp = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ND == 3) kp = *reinterpret_cast<const float4*>(sObsThr + MP + o0 + o4);
+            const float kpv[4] = {kp.x, kp.y, kp.z, kp.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float* ob = obase + (size_t)(o0 + o4 + u) * ND2;
+              const float4 v = *reinterpret_cast<const float4*>(ob);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+              float2 q = __ffma2_rn(dy, dy, make_float2(-thv[u], -thv[u]));
+              q = __ffma2_rn(dx, dx, q);
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(ob + 4);
+                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(kpv[u], kpv[u])), dz, q);
+              }
+              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << (o4 + u);
             }
-            const unsigned hit = (__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31;
-            mask |= hit << o;
           }
+          if (oc < 32) mask &= (1u << oc) - 1u;
         } else {
-          mask = (oc == 32) ? FULL : ((1u << oc) - 1u);
+          const int ov = max(0, min(32, m - o0));
+          mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
         }
         if (!live) mask = 0u;
-        c_screen += (unsigned long long)oc * nsteps;
+        if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
         while (mask) {
           const int o = o0 + __ffs(mask) - 1;
           mask &= mask - 1u;
@@ -472,7 +512,9 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
               const int k = 2 * kg + kk;
               double d[ND], r[ND];
 #pragma unroll
-              for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - __ldg(opos + ((size_t)a * m + o) * K1 + k);
+              for (int a = 0; a < ND; ++a)
+                d[a] = p[a][kk] - (P.obs_static ? sObsC[o * ND + a]
+                                                : __ldg(opos + ((size_t)a * m + o) * K1 + k));
               ++c_exact;
               if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
                 ++c_active;
@@ -683,5 +725,7 @@ __global__ void __launch_bounds__(NT) sf_solve_kernel(const KParams P) {
     }
   }
 }
+
+using KernelFn = void (*)(const KParams);
 
 }  // namespace sfb

@@ -272,11 +272,16 @@ class KktCache:
 # ---------------------------------------------------------------- device batch
 
 
-def _as_tensor(x, device, dtype):
+def _as_tensor(x, device, dtype, counter=None):
     import torch
     if isinstance(x, torch.Tensor):
+        if counter is not None and x.device.type == "cpu":
+            counter[0] += x.numel() * torch.empty(0, dtype=dtype).element_size()
         return x.to(device=device, dtype=dtype).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype).to(device)
+    t = torch.as_tensor(np.ascontiguousarray(x), dtype=dtype)
+    if counter is not None:
+        counter[0] += t.numel() * t.element_size()
+    return t.to(device)
 
 
 class DeviceBatch:
@@ -307,18 +312,19 @@ class DeviceBatch:
         self.kind, self.cfg = kind, cfg
         n, n_d, n_xi = sd0.n, sd0.n_d, sd0.n_basis
         f64, dev = torch.float64, self.device
-        self.xi0 = _as_tensor(xi0, dev, f64)
+        h2d = [0]
+        self.xi0 = _as_tensor(xi0, dev, f64, h2d)
         B = self.xi0.shape[0]
         if tuple(self.xi0.shape) != (B, n_d, n, n_xi):
             raise ShapeError(f"xi0 has shape {tuple(self.xi0.shape)}, expected (B, {n_d}, {n}, {n_xi})")
         self.B = B
-        self.lam0 = (torch.zeros_like(self.xi0) if lam0 is None else _as_tensor(lam0, dev, f64))
+        self.lam0 = (torch.zeros_like(self.xi0) if lam0 is None else _as_tensor(lam0, dev, f64, h2d))
         if tuple(self.lam0.shape) != tuple(self.xi0.shape):
             raise ShapeError("lam0 shape differs from xi0")
         if kind == "projection":
             if target is None:
                 raise ShapeError("projection mode needs a target")
-            self.target = _as_tensor(target, dev, f64)
+            self.target = _as_tensor(target, dev, f64, h2d)
             if tuple(self.target.shape) != tuple(self.xi0.shape):
                 raise ShapeError("target shape differs from xi0")
         else:
@@ -330,12 +336,15 @@ class DeviceBatch:
         mi = np.asarray(member_instance, np.int32)
         if mi.shape != (B,) or mi.min(initial=0) < 0 or mi.max(initial=0) >= len(sds):
             raise ShapeError("member_instance out of range")
-        self.member_instance = torch.as_tensor(mi).to(dev)
-        self.bvals = _as_tensor(np.stack([s.bvals for s in sds]), dev, f64)
-        self.box = _as_tensor(np.stack([s.box for s in sds]), dev, f64)
-        self.obs_pos = _as_tensor(np.stack([s.obs_pos for s in sds]), dev, f64)
-        self.obs_axes = _as_tensor(np.stack([s.obs_axes for s in sds]), dev, f64)
-        self.pair_axes = _as_tensor(np.stack([s.pair_axes for s in sds]), dev, f64)
+        self.member_instance = _as_tensor(mi, dev, torch.int32, h2d)
+        self.bvals = _as_tensor(np.stack([s.bvals for s in sds]), dev, f64, h2d)
+        self.box = _as_tensor(np.stack([s.box for s in sds]), dev, f64, h2d)
+        obs_np = np.stack([s.obs_pos for s in sds])
+        self.obs_static = bool(obs_np.size == 0 or np.all(obs_np == obs_np[..., :1]))
+        self.obs_pos = _as_tensor(obs_np, dev, f64, h2d)
+        self.obs_axes = _as_tensor(np.stack([s.obs_axes for s in sds]), dev, f64, h2d)
+        self.pair_axes = _as_tensor(np.stack([s.pair_axes for s in sds]), dev, f64, h2d)
+        self.h2d_bytes = h2d[0]
         self.n_instances = len(sds)
         d_max = {s.d_max for s in sds}
         if len(d_max) != 1:
@@ -357,7 +366,8 @@ class DeviceBatch:
         p = lambda t: None if t is None else t.data_ptr()
         self._batch = _lib.Batch(self.B, self.n_instances, p(self.member_instance), p(self.xi0),
                                  p(self.lam0), p(self.target), p(self.bvals), p(self.box),
-                                 p(self.obs_pos), p(self.obs_axes), p(self.pair_axes))
+                                 p(self.obs_pos), p(self.obs_axes), p(self.pair_axes),
+                                 _lib.BATCH_STATIC_OBSTACLES if self.obs_static else 0)
         c = self.cfg
         self._cfg = _lib.Config(float(c.rho), float(c.primal_tol), float(c.fp_tol),
                                 float(self.d_max), int(c.max_iters), 1 if self.early_exit else 0)
@@ -376,6 +386,8 @@ class DeviceBatch:
     def results(self) -> dict:
         """Copy results to the host (synchronizes). Member-major arrays."""
         its = self.out_its.cpu().numpy()
+        d2h = its.nbytes + sum(t.numel() * t.element_size() for t in
+                               (self.out_xi, self.out_lam, self.out_primal, self.out_eq, self.out_status))
         out = {
             "xi": self.out_xi.cpu().numpy(), "lam": self.out_lam.cpu().numpy(),
             "primal": self.out_primal.cpu().numpy(), "eq_max": self.out_eq.cpu().numpy(),
@@ -384,9 +396,11 @@ class DeviceBatch:
         if self.out_trace is not None:
             T = int(its.max()) + 1 if its.size else 0
             tr = self.out_trace[:, :T].cpu().numpy()
+            d2h += tr.nbytes
             out["trace"] = [tr[b, : its[b] + 1] for b in range(self.B)]
         if self.out_counters is not None:
             out["counters"] = self.out_counters.cpu().numpy()
+        out["d2h_bytes"] = d2h
         return out
 
 
@@ -507,7 +521,8 @@ def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projectio
     return BatchResult(xi=out["xi"], lam=out["lam"], status=out["status"],
                        iterations=out["iterations"], primal=out["primal"],
                        eq_violation_max=out["eq_max"], trace=out.get("trace"),
-                       wall_time=time.perf_counter() - t0)
+                       wall_time=time.perf_counter() - t0,
+                       extra={"h2d_bytes": batch.h2d_bytes, "d2h_bytes": out["d2h_bytes"]})
 
 
 def cold_start(scn, sys) -> SolverState:
