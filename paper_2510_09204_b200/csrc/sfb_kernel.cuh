@@ -7,8 +7,9 @@
 // the exact rewrites of DESIGN.md §3 (oracle/sf_kron.py is the FP64 restatement):
 //
 //  A  positions   p_i(k) = sum_c W[k,c] xi_i,c in FP64           (constraints.py:159-163)
-//  B  screening   FP32 packed (FFMA2) r^2 test of every pair / obstacle row of the
-//                 lane's robot against a conservative threshold, one bit per body
+//  B  screening   FP32 packed (FADD2/FFMA2) r^2 test of every pair / obstacle row of
+//                 the lane's robot against a conservative threshold, one bit per body
+//                 (funnel-shift accumulation, 2 integer ops per body)
 //  B' exact rows  survivors only: FP64 delta, rho = |delta|_scaled, r1 = delta(1 - clip(rho)/rho)
 //                 (constraints.py:166-247), accumulated into g_i(k) (= F^T r1 rows)
 //  B" box rows    r2 = max(p - p_max, 0) - max(p_min - p, 0) (solver.py:166-168)
@@ -28,20 +29,23 @@
 
 namespace sfb {
 
-constexpr int NW = 8;            // warps per CTA
-constexpr int NT = NW * 32;      // threads per CTA
-constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1) step in shared positions
+#ifndef SFB_MAXW
+#define SFB_MAXW 10
+#endif
+constexpr int NW = SFB_MAXW;     // max warps per CTA (the launch uses P.nw <= NW)
+constexpr int NT = NW * 32;      // max threads per CTA
+constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1 or dummy body) position in shared memory
 constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -> never a hit
 constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the reference evaluates it
 
 struct Layout {       // byte offsets into dynamic shared memory
-  int xi, lam, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs, pmax, uni;
+  int xi, lam, tgt, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs_s, obs, pmax, gl, uni;
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
 };
 
 struct KParams {
-  int n, m, MP, K1, NB, NKG, RB, obs_static;
+  int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
   int mode, max_iters, early_exit;
   double rho, primal_tol, fp_tol, d_max, inv_n;
   float plim;      // FP32 screening valid while max|p| <= plim * (smallest contact axis)
@@ -84,7 +88,12 @@ struct ConstOff {
   }
 };
 
+__host__ __device__ constexpr int nxi_pad(int nxi) { return (nxi + 1) & ~1; }
+
 __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
+
+// append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
+__device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __funnelshift_l(t, m, 1); }
 
 // Exact FP64 residual of one separation row (constraints.py:166-247, trig-free):
 // r1 = delta * (1 - clip(rho, 1, d_max) / rho), coincident rows use alpha = 0, beta = pi/2.
@@ -113,24 +122,54 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
   return true;
 }
 
-// NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
-template <int ND, int NXI, int NJ, bool BIG>
 #ifndef SFB_MINB
 #define SFB_MINB 2
 #endif
+
+// Optional phase timing (build with -DSFB_PHASE_TIMING): thread 0 of every CTA accumulates
+// clock64() deltas per phase into counters[b][4 + phase] (counters must then hold 12 slots).
+#ifdef SFB_PHASE_TIMING
+#define SFB_TMARK(ph)                                   \
+  do {                                                  \
+    if (tid == 0) {                                     \
+      const long long now_ = clock64();                 \
+      t_ph[ph] += now_ - t_last;                        \
+      t_last = now_;                                    \
+    }                                                   \
+  } while (0)
+#define SFB_TSUB(ph)                                    \
+  do {                                                  \
+    if (tid == 0) {                                     \
+      const long long now_ = clock64();                 \
+      t_ph[ph] += now_ - t_sub;                         \
+      t_sub = now_;                                     \
+    }                                                   \
+  } while (0)
+#else
+#define SFB_TMARK(ph) do { } while (0)
+#define SFB_TSUB(ph) do { } while (0)
+#endif
+
+// NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
+template <int ND, int NXI, int NJ, bool BIG>
 __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
+  constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
+  constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = P.nw, nt = nw * 32;
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
-  const int nv = ND * n * NXI;
+  const int nv = ND * n * NXI;       // dense outputs per member
+  const int nrows = ND * n;          // (axis, robot) rows
   const int inst = P.member_instance[b];
 
-  double* sXi = reinterpret_cast<double*>(smem + P.L.xi);
-  double* sLam = reinterpret_cast<double*>(smem + P.L.lam);
+  double* sXi = reinterpret_cast<double*>(smem + P.L.xi);    // [ND*n][NXP]
+  double* sLam = reinterpret_cast<double*>(smem + P.L.lam);  // [ND*n][NXP]
+  double* sTgt = reinterpret_cast<double*>(smem + P.L.tgt);  // [ND*n][NXI] (projection target)
   double* sW = reinterpret_cast<double*>(smem + P.L.w);      // [NKG][NXI][2]
   double* sE = reinterpret_cast<double*>(smem + P.L.e);      // [NB][NXI]
   double* sQ = reinterpret_cast<double*>(smem + P.L.q);      // [NXI][NXI]
@@ -138,57 +177,71 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   double* sPxb = reinterpret_cast<double*>(smem + P.L.pxb);
   double* sDxx = reinterpret_cast<double*>(smem + P.L.dxx);
   double* sDxb = reinterpret_cast<double*>(smem + P.L.dxb);
-  double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND][n][NXI]
-  double* sBv = reinterpret_cast<double*>(smem + P.L.bv);    // [ND][n][NB]
+  double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND*n][NXI]
+  double* sBv = reinterpret_cast<double*>(smem + P.L.bv);    // [ND*n][NB]
   double* sRed = reinterpret_cast<double*>(smem + P.L.red);  // [NW][4] + misc
   double* sObsAx = reinterpret_cast<double*>(smem + P.L.obs_ax);   // [MP][4] inv_a2 inv_b2 a b
   float* sObsThr = reinterpret_cast<float*>(smem + P.L.obs_thr);   // [2][MP] thr, kappa
   double* sObsC = reinterpret_cast<double*>(smem + P.L.obs_c);     // [MP][ND] exact centers (static)
-  float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [static ? 1 : NKG][MP][ND2]
+  float* sObsS = reinterpret_cast<float*>(smem + P.L.obs_s);       // [MP][OS] static: -x -y (-z) -thr (kappa)
+  float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [NKG][MP][ND2] (dynamic)
   float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [NKG][8] (n > 32)
   unsigned char* uni = smem + P.L.uni;
-  constexpr int dummy_nj = NJ;
-  (void)dummy_nj;
   const int NROW = BIG ? n : NJ;                                    // bodies per k-group row
-  float* sPos = reinterpret_cast<float*>(uni);                      // [NKG][NROW][ND2] hi
+  // n > 32: positions of every k-group are shared by the robot-block warps of that k-group;
+  // n <= 32: a warp holds all robots of its k-groups, so it owns a private position row
+  float* sPos = reinterpret_cast<float*>(uni);                      // BIG [NKG][NROW][ND2] / [nw][32/NJ][NJ][ND2]
   float* sLo = sPos + (size_t)NKG * NROW * ND2;                     // [NKG][NROW][ND2] lo (BIG)
-  double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots
-  // KKT scratch (aliases the union region after the contraction)
-  double* sD = reinterpret_cast<double*>(uni);                      // [ND][n][NXI]
-  double* sU = sD + nv;                                             // [ND][n][NB]
+  double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots (BIG)
+  // n <= 32: per-lane G partials [nw][NXI][ND][32] (conflict-free, lane-contiguous)
+  double* sGl = reinterpret_cast<double*>(smem + P.L.gl);
+  // KKT scratch (aliases the union region (BIG) / the per-lane partials after the reduction)
+  double* sD = reinterpret_cast<double*>(BIG ? uni : smem + P.L.gl);  // [ND*n][NXI]
+  double* sU = sD + nv;                                             // [ND*n][NB]
   double* sSD = sU + ND * n * NB;                                   // [ND][NXI]
   double* sSU = sSD + ND * NXI;                                     // [ND][NB]
 
   const ConstOff co = ConstOff::make(K1, NXI, NB);
+  // (axis, robot) row of a dense index o = ai * NXI + c without runtime division
+  auto split = [&](int o, int& ai, int& c, int& a, int& ii) {
+    ai = o / NXI;
+    c = o - ai * NXI;
+    a = (ai >= n) + (ND == 3 && ai >= 2 * n);
+    ii = ai - a * n;
+  };
 
   // ------------------------------------------------------------------ setup
-  for (int idx = tid; idx < NKG * NXI * 2; idx += NT) {
+  for (int idx = tid; idx < NKG * NXI * 2; idx += nt) {
     const int kg = idx / (NXI * 2), rem = idx - kg * NXI * 2, c = rem >> 1, kk = rem & 1;
     const int k = 2 * kg + kk;
     sW[idx] = (k < K1) ? P.consts[co.W + k * NXI + c] : 0.0;
   }
-  for (int idx = tid; idx < NB * NXI; idx += NT) sE[idx] = P.consts[co.E + idx];
-  for (int idx = tid; idx < NXI * NXI; idx += NT) {
+  for (int idx = tid; idx < NB * NXI; idx += nt) sE[idx] = P.consts[co.E + idx];
+  for (int idx = tid; idx < NXI * NXI; idx += nt) {
     sQ[idx] = P.consts[co.Q + idx];
     sPxx[idx] = P.consts[co.Pxx + idx];
     sDxx[idx] = P.consts[co.Dxx + idx];
   }
-  for (int idx = tid; idx < NXI * NB; idx += NT) {
+  for (int idx = tid; idx < NXI * NB; idx += nt) {
     sPxb[idx] = P.consts[co.Pxb + idx];
     sDxb[idx] = P.consts[co.Dxb + idx];
   }
   {
     const double* x0 = P.xi0 + (size_t)b * nv;
     const double* l0 = P.lam0 + (size_t)b * nv;
-    for (int idx = tid; idx < nv; idx += NT) {
-      sXi[idx] = x0[idx];
-      sLam[idx] = l0[idx];
+    const double* t0 = P.target ? P.target + (size_t)b * nv : nullptr;
+    for (int o = tid; o < nv; o += nt) {
+      const int ai = o / NXI, c = o - ai * NXI;
+      sXi[ai * NXP + c] = x0[o];
+      sLam[ai * NXP + c] = l0[o];
+      sTgt[o] = t0 ? t0[o] : 0.0;
     }
     const double* bv = P.bvals + (size_t)inst * ND * n * NB;
-    for (int idx = tid; idx < ND * n * NB; idx += NT) sBv[idx] = bv[idx];
+    for (int idx = tid; idx < ND * n * NB; idx += nt) sBv[idx] = bv[idx];
   }
   // obstacles, padded to MP (multiple of 4) with far-away dummies that never screen in
-  for (int o = tid; o < MP; o += NT) {
+  for (int o = tid; o < MP; o += nt) {
+    float* st = sObsS + o * OS;
     if (o < m) {
       const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
       const double a = oa[0], bb = oa[2];
@@ -196,38 +249,51 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       sObsAx[o * 4 + 1] = 1.0 / (bb * bb);
       sObsAx[o * 4 + 2] = a;
       sObsAx[o * 4 + 3] = bb;
-      sObsThr[o] = (float)(a * a * (1.0 + 2e-3));
-      sObsThr[MP + o] = (float)((a * a) / (bb * bb));
+      const float thr = (float)(a * a * (1.0 + 2e-3)), kap = (float)((a * a) / (bb * bb));
+      sObsThr[o] = thr;
+      sObsThr[MP + o] = kap;
 #pragma unroll
-      for (int a2 = 0; a2 < ND; ++a2) sObsC[o * ND + a2] = P.obs_pos[(((size_t)inst * ND + a2) * m + o) * K1];
+      for (int a2 = 0; a2 < ND; ++a2) {
+        const double c0 = P.obs_pos[(((size_t)inst * ND + a2) * m + o) * K1];
+        sObsC[o * ND + a2] = c0;
+        st[a2] = -(float)c0;
+      }
+      st[ND] = -thr;
+      if (ND == 3) { st[4] = kap; st[5] = st[6] = st[7] = 0.f; } else { st[3] = 0.f; }
     } else {
       sObsThr[o] = 0.f;
       sObsThr[MP + o] = 0.f;
+#pragma unroll
+      for (int a2 = 0; a2 < OS; ++a2) st[a2] = 0.f;
+      st[0] = -PAD_SMEM;                     // dummy at +3e30: never within any threshold
     }
   }
   float obs_absmax = 0.f, obs_axmin = INFINITY;
-  for (int o = tid; o < m; o += NT) {
+  for (int o = tid; o < m; o += nt) {
     const double* oa = P.obs_axes + ((size_t)inst * m + o) * 3;
     obs_axmin = fminf(obs_axmin, (float)(ND == 3 ? fmin(oa[0], oa[2]) : oa[0]));
   }
-  const int NKGO = P.obs_static ? 1 : NKG;
-  for (int idx = tid; idx < NKGO * MP; idx += NT) {
+  const int NKGO = P.obs_static ? 0 : NKG;
+  for (int idx = tid; idx < NKGO * MP; idx += nt) {
     const int kg = idx / MP, o = idx - kg * MP;
     float* dst = sObs + (size_t)idx * ND2;
 #pragma unroll
     for (int a = 0; a < ND; ++a) {
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        const int k = P.obs_static ? 0 : 2 * kg + kk;
+        const int k = 2 * kg + kk;
         float v = PAD_SMEM;
-        if (o < m && k < K1) {
-          v = (float)P.obs_pos[(((size_t)inst * ND + a) * m + o) * K1 + k];
-          obs_absmax = fmax_abs(obs_absmax, v);
-        }
+        if (o < m && k < K1) v = (float)P.obs_pos[(((size_t)inst * ND + a) * m + o) * K1 + k];
         dst[a * 2 + kk] = v;
       }
     }
     if (ND == 3) dst[6] = dst[7] = 0.f;
+  }
+  for (int idx = tid; idx < m * K1; idx += nt) {
+    const int o = idx / K1, k = idx - o * K1;
+#pragma unroll
+    for (int a = 0; a < ND; ++a)
+      obs_absmax = fmax_abs(obs_absmax, (float)P.obs_pos[(((size_t)inst * ND + a) * m + o) * K1 + k]);
   }
   unsigned* sMisc = reinterpret_cast<unsigned*>(sRed + NW * 4);
   if (tid == 0) {
@@ -252,51 +318,49 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   const float r_kap = (float)((ra * ra) / (rb_ax * rb_ax));
   const double d_max = P.d_max;
   // FP32 positions carry ~2^-24 |p| error: the screen margin (1e-3 of the contact
-  // distance) covers it while every |p| <= plim (DESIGN.md §4.2); beyond, rows go exact
+  // distance) covers it while every |p| <= plim (DESIGN.md §4); beyond, rows go exact
   const float plim = P.plim * fminf(__uint_as_float(sMisc[1]),
                                     (float)(ND == 3 ? fmin(ra, rb_ax) : ra));
   const double* opos = P.obs_pos + (size_t)inst * ND * m * K1;
-  const double* tgt = P.target ? P.target + (size_t)b * nv : nullptr;
 
   // lane -> (robot, k-group) mapping
   constexpr int LW = BIG ? 32 : NJ, SUB = 32 / LW;
   int sub, rbk, wk, nwk;
   if (BIG) {
     sub = 0;
-    rbk = warp % P.RB; wk = warp / P.RB; nwk = NW / P.RB;
+    rbk = warp & (P.RB - 1); wk = warp / P.RB; nwk = nw / P.RB;
   } else {
     sub = lane / LW;
-    rbk = 0; wk = warp; nwk = NW;
+    rbk = 0; wk = warp; nwk = nw;
   }
   const int i = BIG ? rbk * 32 + lane : lane % LW;
   const bool robot_ok = i < n;
   const int ic = robot_ok ? i : n - 1;
   const int NTS = (NKG + SUB - 1) / SUB;
+  const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
 
+#ifdef SFB_PHASE_TIMING
+  long long t_ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_last = clock64(), t_sub = t_last;
+#endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   double eq_max = 0.0;
   unsigned long long c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
   for (int it = 0;; ++it) {
-    // -------------------------------------------- eq violation of the committed xi
-    double eqp = 0.0;
-    if (it > 0) {
-      for (int idx = tid; idx < ND * n * NB; idx += NT) {
-        const int a = idx / (n * NB), rem = idx - a * n * NB, ii = rem / NB, r = rem - ii * NB;
-        const double* x = sXi + (a * n + ii) * NXI;
-        double v = 0.0;
-#pragma unroll
-        for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-        eqp = fmax(eqp, fabs(v - sBv[idx]));
-      }
-    }
-
     // -------------------------------------------- A/B/C per k-group task
-    double Gp[ND][NXI];
+    double Gp[BIG ? ND : 1][BIG ? NXI : 1];
+    double* gl = sGl + (size_t)warp * NXI * ND * 32 + lane;          // this lane's partials, stride 32
+    if (BIG) {
 #pragma unroll
-    for (int a = 0; a < ND; ++a)
+      for (int a = 0; a < (BIG ? ND : 1); ++a)
 #pragma unroll
-      for (int c = 0; c < NXI; ++c) Gp[a][c] = 0.0;
+        for (int c = 0; c < (BIG ? NXI : 1); ++c) Gp[a][c] = 0.0;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NXI * ND; ++q) gl[q * 32] = 0.0;
+    }
+    float* posw = sPos + (size_t)(warp * SUB + sub) * NJ * ND2;        // !BIG: this k-group's row
     double s1 = 0.0, s2 = 0.0;
 
     for (int ts = wk; ts < NTS; ts += nwk) {
@@ -306,19 +370,31 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       const bool live = robot_ok && kg_ok;
       const bool has1 = 2 * kg + 1 < K1;
       const double2* wk2 = reinterpret_cast<const double2*>(sW + (size_t)kg * NXI * 2);
+#ifdef SFB_PHASE_TIMING
+      if (tid == 0) t_sub = clock64();
+#endif
 
       // A: exact positions of the lane's robot at the two steps
       double p[ND][2];
 #pragma unroll
       for (int a = 0; a < ND; ++a) p[a][0] = p[a][1] = 0.0;
 #pragma unroll
-      for (int c = 0; c < NXI; ++c) {
-        const double2 w = wk2[c];
+      for (int c = 0; c + 1 < NXI; c += 2) {
+        const double2 w0 = wk2[c], w1 = wk2[c + 1];
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
-          const double x = sXi[(a * n + ic) * NXI + c];
-          p[a][0] = fma(w.x, x, p[a][0]);
-          p[a][1] = fma(w.y, x, p[a][1]);
+          const double2 x = *reinterpret_cast<const double2*>(xrow + a * n * NXP + c);
+          p[a][0] = fma(w1.x, x.y, fma(w0.x, x.x, p[a][0]));
+          p[a][1] = fma(w1.y, x.y, fma(w0.y, x.x, p[a][1]));
+        }
+      }
+      if (NXI & 1) {
+        const double2 w0 = wk2[NXI - 1];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+          const double x = xrow[a * n * NXP + NXI - 1];
+          p[a][0] = fma(w0.x, x, p[a][0]);
+          p[a][1] = fma(w0.y, x, p[a][1]);
         }
       }
       float own[ND][2];
@@ -336,8 +412,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           own[a][1] = (live && has1) ? h1 : PAD_OWN;
         }
         if (ND == 3) hv[6] = hv[7] = 0.f;
-        if (kg_ok && (!BIG || robot_ok)) {
-          float4* dst = reinterpret_cast<float4*>(sPos + ((size_t)kg * NROW + i) * ND2);
+        if (BIG ? (kg_ok && robot_ok) : true) {
+          float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)kg * NROW + i) * ND2 : posw + i * ND2);
           dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
           if (BIG) {
@@ -369,6 +445,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       const float2 ny = make_float2(-own[1][0], -own[1][1]);
       const float2 nz = (ND == 3) ? make_float2(-own[ND - 1][0], -own[ND - 1][1]) : make_float2(0.f, 0.f);
       const int nsteps = live ? (has1 ? 2 : 1) : 0;
+      SFB_TSUB(6);
 
       double g[ND][2];
 #pragma unroll
@@ -380,44 +457,40 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         unsigned mask = 0u;
         if (!force) {
           const float2 thr2 = make_float2(-r_thr, -r_thr);
-          const float* base = sPos + ((size_t)kg * NROW + j0) * ND2;
+          const float* base = BIG ? sPos + ((size_t)kg * NROW + j0) * ND2 : posw;
+          unsigned mm = 0u;
+          auto screen = [&](const float* bp) {
+            const float4 v = *reinterpret_cast<const float4*>(bp);
+            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+            float2 q = __ffma2_rn(dy, dy, thr2);
+            q = __ffma2_rn(dx, dx, q);
+            if (ND == 3) {
+              const float4 v2 = *reinterpret_cast<const float4*>(bp + 4);
+              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+              q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
+            }
+            mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+          };
           if (BIG) {
 #pragma unroll 4
-            for (int j = 0; j < jc; ++j) {
-              const float4 v = *reinterpret_cast<const float4*>(base + (size_t)j * ND2);
-              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-              float2 q = __ffma2_rn(dy, dy, thr2);
-              q = __ffma2_rn(dx, dx, q);
-              if (ND == 3) {
-                const float4 v2 = *reinterpret_cast<const float4*>(base + (size_t)j * ND2 + 4);
-                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-                q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
-              }
-              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << j;
-            }
+            for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2);
+            mask = __brev(mm) >> (32 - jc);
           } else {
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-              const float4 v = *reinterpret_cast<const float4*>(base + j * ND2);
-              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-              float2 q = __ffma2_rn(dy, dy, thr2);
-              q = __ffma2_rn(dx, dx, q);
-              if (ND == 3) {
-                const float4 v2 = *reinterpret_cast<const float4*>(base + j * ND2 + 4);
-                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-                q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
-              }
-              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << j;
-            }
+            for (int j = 0; j < NJ; ++j) screen(base + j * ND2);
+            mask = (__brev(mm) >> (32 - NJ)) & ((jc >= 32) ? FULL : ((1u << jc) - 1u));
           }
         } else {
           mask = (jc >= 32) ? FULL : ((1u << jc) - 1u);
         }
         if (i >= j0 && i < j0 + jc) mask &= ~(1u << (i - j0));
         if (!live) mask = 0u;
+#ifdef SFB_EXP_NOEXACT
+        if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;   // timing ablation only
+#endif
         if (P.counters) c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
+        SFB_TSUB(7);
 
         // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)
         while (__any_sync(FULL, mask != 0u)) {
@@ -466,41 +539,66 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
       }
 
+      SFB_TSUB(8);
       // B: obstacles (padded to MP), in chunks of 32
-      const float* obase = sObs + (P.obs_static ? 0 : (size_t)kg * MP * ND2);
+#ifdef SFB_EXP_NOOBS
+      for (int o0 = 0; o0 < 0; o0 += 32) {
+#else
       for (int o0 = 0; o0 < MP; o0 += 32) {
+#endif
         const int oc = min(32, MP - o0);
         unsigned mask = 0u;
         if (!force) {
-#pragma unroll 2
-          for (int o4 = 0; o4 < oc; o4 += 4) {
-            const float4 th = *reinterpret_cast<const float4*>(sObsThr + o0 + o4);
-            const float thv[4] = {th.x, th.y, th.z, th.w};
-            float4 kp = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ND == 3) kp = *reinterpret_cast<const float4*>(sObsThr + MP + o0 + o4);
-            const float kpv[4] = {kp.x, kp.y, kp.z, kp.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float* ob = obase + (size_t)(o0 + o4 + u) * ND2;
-              const float4 v = *reinterpret_cast<const float4*>(ob);
+          unsigned mm = 0u;
+          if (P.obs_static) {
+            // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
+            const float* ob = sObsS + (size_t)o0 * OS;
+#pragma unroll 4
+            for (int o = 0; o < oc; ++o) {
+              const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
+              const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
+              float2 q;
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(ob + o * OS + 4);
+                const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
+                                             make_float2(own[ND - 1][0], own[ND - 1][1]));
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
+                q = __ffma2_rn(dy, dy, q);
+              } else {
+                q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
+              }
+              q = __ffma2_rn(dx, dx, q);
+              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+            }
+          } else {
+            const float* obase = sObs + ((size_t)kg * MP + o0) * ND2;
+#pragma unroll 4
+            for (int o = 0; o < oc; ++o) {
+              const float4 v = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2);
+              const float th = sObsThr[o0 + o];
               const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
               const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-              float2 q = __ffma2_rn(dy, dy, make_float2(-thv[u], -thv[u]));
+              float2 q = __ffma2_rn(dy, dy, make_float2(-th, -th));
               q = __ffma2_rn(dx, dx, q);
               if (ND == 3) {
-                const float4 v2 = *reinterpret_cast<const float4*>(ob + 4);
+                const float kp = sObsThr[MP + o0 + o];
+                const float4 v2 = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2 + 4);
                 const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-                q = __ffma2_rn(__fmul2_rn(dz, make_float2(kpv[u], kpv[u])), dz, q);
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(kp, kp)), dz, q);
               }
-              mask |= ((__float_as_uint(q.x) | __float_as_uint(q.y)) >> 31) << (o4 + u);
+              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
             }
           }
-          if (oc < 32) mask &= (1u << oc) - 1u;
+          mask = __brev(mm) >> (32 - oc);
         } else {
           const int ov = max(0, min(32, m - o0));
           mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
         }
         if (!live) mask = 0u;
+#ifdef SFB_EXP_NOEXACT
+        if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
+#endif
         if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
         while (mask) {
           const int o = o0 + __ffs(mask) - 1;
@@ -531,6 +629,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
       }
 
+      SFB_TSUB(9);
       // B": workspace box rows (exact, every step)
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
@@ -551,52 +650,70 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         for (int c = 0; c < NXI; ++c) {
           const double2 w = wk2[c];
 #pragma unroll
-          for (int a = 0; a < ND; ++a) Gp[a][c] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[a][c]));
+          for (int a = 0; a < ND; ++a) {
+            if (BIG) {
+              Gp[BIG ? a : 0][BIG ? c : 0] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[BIG ? a : 0][BIG ? c : 0]));
+            } else {
+              double* q = gl + (c * ND + a) * 32;
+              *q = fma(w.x, g[a][0], fma(w.y, g[a][1], *q));
+            }
+          }
         }
       }
-      if (BIG) __syncwarp();
+      __syncwarp();   // the next task overwrites this warp's position row
+      SFB_TSUB(10);
     }
 
     // -------------------------------------------- reductions
-    if (!BIG) {
-      for (int off = LW; off < 32; off <<= 1) {
-#pragma unroll
-        for (int a = 0; a < ND; ++a)
-#pragma unroll
-          for (int c = 0; c < NXI; ++c) Gp[a][c] += __shfl_xor_sync(FULL, Gp[a][c], off);
-      }
-    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       s1 += __shfl_xor_sync(FULL, s1, off);
       s2 += __shfl_xor_sync(FULL, s2, off);
-      eqp = fmax(eqp, __shfl_xor_sync(FULL, eqp, off));
     }
     if (lane == 0) {
       sRed[warp * 4 + 0] = s1;
       sRed[warp * 4 + 1] = s2;
-      sRed[warp * 4 + 2] = eqp;
     }
+    SFB_TMARK(0);
     __syncthreads();   // all positions consumed: the union region is free
+    SFB_TMARK(1);
 
-    // G partials: slot s of round r holds warp r*slots + s, layout [ND][32][NXI]
-    const int slots = P.L.slots;
-    for (int w0 = 0; w0 < NW; w0 += slots) {
-      if (warp >= w0 && warp < w0 + slots && (BIG ? true : sub == 0) && robot_ok) {
-        double* dst = sSlot + (size_t)(warp - w0) * ND * 32 * NXI;
-        const int li = BIG ? lane : i;
+    if (!BIG) {
+      // G = sum over warps, then over the k-group sub-lanes, of the per-lane partials (fixed order)
+      // thread = (column (c, a), robot): consecutive threads read consecutive lanes
+      for (int o = tid; o < NXI * ND * 32; o += nt) {
+        const int ii = o & 31, col = o >> 5;
+        if (ii >= n) continue;
+        const int c = col / ND, a = col - c * ND;
+        double acc = 0.0;
+        for (int w = 0; w < nw; ++w) {
+          const double* src = sGl + (size_t)(w * NXI * ND + col) * 32 + ii;
 #pragma unroll
-        for (int a = 0; a < ND; ++a)
-#pragma unroll
-          for (int c = 0; c < NXI; ++c) dst[(a * 32 + li) * NXI + c] = Gp[a][c];
+          for (int s2i = 0; s2i < SUB; ++s2i) acc += src[s2i * NJ];
+        }
+        sG[(a * n + ii) * NXI + c] = acc;
       }
       __syncthreads();
-      for (int o = tid; o < nv; o += NT) {
-        const int a = o / (n * NXI), rem = o - a * n * NXI, ii = rem / NXI, c = rem - ii * NXI;
+    }
+    // n > 32: G partials in slots; slot s of round r holds warp r*slots + s, layout [ND][32][NXI]
+    const int slots = P.L.slots;
+    for (int w0 = 0; BIG && w0 < nw; w0 += slots) {
+      if (warp >= w0 && warp < w0 + slots && robot_ok) {
+        double* dst = sSlot + (size_t)(warp - w0) * ND * 32 * NXI;
+#pragma unroll
+        for (int a = 0; a < (BIG ? ND : 1); ++a)
+#pragma unroll
+          for (int c = 0; c < (BIG ? NXI : 1); ++c) dst[(a * 32 + lane) * NXI + c] = Gp[a][c];
+      }
+      __syncthreads();
+      for (int o = tid; o < nv; o += nt) {
+        int ai, c, a, ii;
+        split(o, ai, c, a, ii);
         const int rbi = ii >> 5, li = ii & 31;
         double acc = (w0 == 0) ? 0.0 : sG[o];
-        for (int w = w0; w < min(NW, w0 + slots); ++w) {
-          if ((BIG ? (w % P.RB) : 0) != rbi) continue;
+        const int wend = min(nw, w0 + slots);
+        for (int w = w0; w < wend; ++w) {
+          if ((BIG ? (w & (P.RB - 1)) : 0) != rbi) continue;
           acc += sSlot[(size_t)(w - w0) * ND * 32 * NXI + (a * 32 + li) * NXI + c];
         }
         sG[o] = acc;
@@ -604,20 +721,16 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       __syncthreads();
     }
 
+    SFB_TMARK(2);
     // -------------------------------------------- D: residuals, trace, convergence
-    double S1 = 0.0, S2 = 0.0, EQ = 0.0, FP = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    double S1 = 0.0, S2 = 0.0, FP = 0.0;
+    for (int w = 0; w < nw; ++w) {
       S1 += sRed[w * 4 + 0];
       S2 += sRed[w * 4 + 1];
-      EQ = fmax(EQ, sRed[w * 4 + 2]);
       FP += sRed[w * 4 + 3];
     }
     const double primal = sqrt(S1) + sqrt(S2);
-    if (it > 0) {
-      last_fp = FP;
-      eq_max = fmax(eq_max, EQ);
-    }
+    if (it > 0) last_fp = FP;
     ++c_evals;
     if (tid == 0 && P.trace) {
       double* tr = P.trace + ((size_t)b * (P.max_iters + 1) + it) * 2;
@@ -627,11 +740,30 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     const bool conv_p = P.early_exit && (primal < P.primal_tol) && it >= 1;
     const bool conv_f = P.early_exit && (last_fp < P.fp_tol);
     if (conv_p || conv_f || it == P.max_iters) {
+      // the xi committed at it-1 has not had its boundary residual measured yet
+      if (it > 0) {
+        double eqp = 0.0;
+        for (int ai = tid; ai < nrows; ai += nt) {
+          const double* x = sXi + ai * NXP;
+          for (int r = 0; r < NB; ++r) {
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+            eqp = fmax(eqp, fabs(v - sBv[ai * NB + r]));
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) eqp = fmax(eqp, __shfl_xor_sync(FULL, eqp, off));
+        if (lane == 0) sRed[warp * 4 + 2] = eqp;
+        __syncthreads();
+        for (int w = 0; w < nw; ++w) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
+      }
       double* xo = P.xi + (size_t)b * nv;
       double* lo = P.lam + (size_t)b * nv;
-      for (int idx = tid; idx < nv; idx += NT) {
-        xo[idx] = sXi[idx];
-        lo[idx] = sLam[idx];
+      for (int o = tid; o < nv; o += nt) {
+        const int ai = o / NXI, c = o - ai * NXI;
+        xo[o] = sXi[ai * NXP + c];
+        lo[o] = sLam[ai * NXP + c];
       }
       if (tid == 0) {
         P.primal[b] = primal;
@@ -642,72 +774,113 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       break;
     }
 
+    SFB_TMARK(3);
     // -------------------------------------------- E: multiplier update and KKT step
-    double fpp = 0.0;
-    for (int o = tid; o < nv; o += NT) {
-      const int ai = o / NXI, c = o - ai * NXI;
-      const double lo = sLam[o];
-      const double ln = fma(-P.rho, sG[o], lo);
-      double qx;
-      if (P.mode == 0) {
-        qx = sXi[o];
+    // E1: one warp per column, lanes = robots. Columns (a, c): lambda+, Delta and the robot
+    // sum of Delta; columns (a, r): u = b - E xi, its robot sum, and max|u| (the boundary
+    // residual of the xi committed at it-1, solver.py:336-337). Sums use a fixed xor tree.
+    double fpp = 0.0, equ = 0.0;
+    const int ncolD = ND * NXI, ncol = ncolD + ND * NB;
+    for (int col = warp; col < ncol; col += nw) {
+      double csum = 0.0;
+      if (col < ncolD) {
+        const int a = col / NXI, c = col - a * NXI;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+          const int ii = i0 + lane;
+          if (ii < n) {
+            const int ai = a * n + ii;
+            const double lo = sLam[ai * NXP + c];
+            const double ln = fma(-P.rho, sG[ai * NXI + c], lo);
+            double qx;
+            if (P.mode == 0) {
+              qx = sXi[ai * NXP + c];
+            } else {
+              qx = 0.0;
+              const double* x = sXi + ai * NXP;
+#pragma unroll
+              for (int c2 = 0; c2 < NXI; ++c2) qx = fma(sQ[c * NXI + c2], x[c2], qx);
+            }
+            const double t = sTgt[ai * NXI + c];
+            const double d = 2.0 * ln - lo + t - qx;
+            sD[ai * NXI + c] = d;
+            sLam[ai * NXP + c] = ln;
+            const double dl = ln - lo;
+            fpp = fma(dl, dl, fpp);
+            csum += d;
+          }
+        }
       } else {
-        qx = 0.0;
-        const double* x = sXi + ai * NXI;
+        const int t2 = col - ncolD, a = t2 / NB, r = t2 - a * NB;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+          const int ii = i0 + lane;
+          if (ii < n) {
+            const int ai = a * n + ii;
+            const double* x = sXi + ai * NXP;
+            double v = 0.0;
 #pragma unroll
-        for (int c2 = 0; c2 < NXI; ++c2) qx = fma(sQ[c * NXI + c2], x[c2], qx);
+            for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+            const double u = sBv[ai * NB + r] - v;
+            sU[ai * NB + r] = u;
+            equ = fmax(equ, fabs(u));
+            csum += u;
+          }
+        }
       }
-      const double t = tgt ? tgt[o] : 0.0;
-      sD[o] = 2.0 * ln - lo + t - qx;
-      sLam[o] = ln;
-      const double dl = ln - lo;
-      fpp = fma(dl, dl, fpp);
-    }
-    for (int idx = tid; idx < ND * n * NB; idx += NT) {
-      const int ai = idx / NB, r = idx - ai * NB;
-      const double* x = sXi + ai * NXI;
-      double v = 0.0;
 #pragma unroll
-      for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-      sU[idx] = sBv[idx] - v;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < ND * (NXI + NB); idx += NT) {
-      const int a = idx / (NXI + NB), cc = idx - a * (NXI + NB);
-      double acc = 0.0;
-      if (cc < NXI) {
-        for (int ii = 0; ii < n; ++ii) acc += sD[(a * n + ii) * NXI + cc];
-        sSD[a * NXI + cc] = acc;
-      } else {
-        const int r = cc - NXI;
-        for (int ii = 0; ii < n; ++ii) acc += sU[(a * n + ii) * NB + r];
-        sSU[a * NB + r] = acc;
+      for (int off = 16; off > 0; off >>= 1) csum += __shfl_xor_sync(FULL, csum, off);
+      if (lane == 0) {
+        if (col < ncolD) sSD[col] = csum;
+        else sSU[col - ncolD] = csum;
       }
     }
-    __syncthreads();
-    for (int o = tid; o < nv; o += NT) {
-      const int ai = o / NXI, c = o - ai * NXI, a = ai / n;
-      const double* dv = sD + ai * NXI;
-      const double* uv = sU + ai * NB;
-      double acc = 0.0;
 #pragma unroll
-      for (int c2 = 0; c2 < NXI; ++c2) acc = fma(sPxx[c * NXI + c2], dv[c2], acc);
-      for (int r = 0; r < NB; ++r) acc = fma(sPxb[c * NB + r], uv[r], acc);
+    for (int off = 16; off > 0; off >>= 1) equ = fmax(equ, __shfl_xor_sync(FULL, equ, off));
+    if (lane == 0) sRed[warp * 4 + 2] = equ;
+    __syncthreads();
+    SFB_TMARK(4);
+    if (it > 0) {
+      for (int w = 0; w < nw; ++w) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
+    }
+    // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp
+    for (int col = warp; col < ncolD; col += nw) {
+      const int a = col / NXI, c = col - a * NXI;
       double mean = 0.0;
 #pragma unroll
       for (int c2 = 0; c2 < NXI; ++c2) mean = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], mean);
       for (int r = 0; r < NB; ++r) mean = fma(sDxb[c * NB + r], sSU[a * NB + r], mean);
-      const double xo = sXi[o];
-      const double xn = xo + (acc + mean);
-      sXi[o] = xn;
-      const double dx = xn - xo;
-      fpp = fma(dx, dx, fpp);
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const int ii = i0 + lane;
+        if (ii < n) {
+          const int ai = a * n + ii;
+          const double* dv = sD + ai * NXI;
+          const double* uv = sU + ai * NB;
+          double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+          for (int c2 = 0; c2 + 1 < NXI; c2 += 2) {
+            acc0 = fma(sPxx[c * NXI + c2], dv[c2], acc0);
+            acc1 = fma(sPxx[c * NXI + c2 + 1], dv[c2 + 1], acc1);
+          }
+          if (NXI & 1) acc0 = fma(sPxx[c * NXI + NXI - 1], dv[NXI - 1], acc0);
+          for (int r = 0; r < NB; ++r) acc1 = fma(sPxb[c * NB + r], uv[r], acc1);
+          const double xo = sXi[ai * NXP + c];
+          const double xn = xo + ((acc0 + acc1) + mean);
+          sXi[ai * NXP + c] = xn;
+          const double dx = xn - xo;
+          fpp = fma(dx, dx, fpp);
+        }
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) fpp += __shfl_xor_sync(FULL, fpp, off);
     if (lane == 0) sRed[warp * 4 + 3] = fpp;
     __syncthreads();
+    SFB_TMARK(5);
   }
+#ifdef SFB_PHASE_TIMING
+  if (tid == 0 && P.counters) {
+    for (int q = 0; q < 11; ++q) P.counters[(size_t)b * 16 + 4 + q] = (unsigned long long)t_ph[q];
+  }
+#endif
 
   if (P.counters) {
 #pragma unroll
@@ -717,7 +890,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       c_screen += __shfl_xor_sync(FULL, c_screen, off);
     }
     if (lane == 0) {
+#ifdef SFB_PHASE_TIMING
+      unsigned long long* cb = P.counters + (size_t)b * 16;
+#else
       unsigned long long* cb = P.counters + (size_t)b * 4;
+#endif
       atomicAdd(cb + 0, c_exact);
       atomicAdd(cb + 1, c_active);
       atomicAdd(cb + 2, c_screen);

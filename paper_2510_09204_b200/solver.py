@@ -227,8 +227,9 @@ class Plan:
 
     def __del__(self):
         ptr = getattr(self, "_ptr", None)
-        if ptr is not None and ptr.value and _lib._LIB is not None:
-            _lib._LIB.sfb_plan_destroy(ptr)
+        L = getattr(_lib, "_LIB", None) if _lib is not None else None
+        if ptr is not None and ptr.value and L is not None:
+            L.sfb_plan_destroy(ptr)
             self._ptr = None
 
 
