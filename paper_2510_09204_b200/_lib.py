@@ -39,7 +39,8 @@ BATCH_STATIC_OBSTACLES = 1
 class Config(ctypes.Structure):
     _fields_ = [("rho", ctypes.c_double), ("primal_tol", ctypes.c_double),
                 ("fp_tol", ctypes.c_double), ("d_max", ctypes.c_double),
-                ("max_iters", ctypes.c_int32), ("early_exit", ctypes.c_int32)]
+                ("max_iters", ctypes.c_int32), ("early_exit", ctypes.c_int32),
+                ("cluster", ctypes.c_int32)]
 
 
 class Out(ctypes.Structure):

@@ -24,13 +24,14 @@
 // positions with a warp-broadcast LDS.128; the partner's exact FP64 position comes
 // from its owner lane by shuffle (n <= 32) or from FP32 hi/lo pairs in smem (n > 32).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace sfb {
 
 #ifndef SFB_MAXW
-#define SFB_MAXW 10
+#define SFB_MAXW 8
 #endif
 constexpr int NW = SFB_MAXW;     // max warps per CTA (the launch uses P.nw <= NW)
 constexpr int NT = NW * 32;      // max threads per CTA
@@ -40,12 +41,14 @@ constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the refer
 
 struct Layout {       // byte offsets into dynamic shared memory
   int xi, lam, tgt, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs_s, obs, pmax, gl, uni;
+  int xg;             // cluster exchange buffers [2][nv + 2] (set at launch when csize > 1)
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
 };
 
 struct KParams {
   int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
+  int csize;       // CTAs per member (thread-block cluster along the time axis), 1..8
   int mode, max_iters, early_exit;
   double rho, primal_tol, fp_tol, d_max, inv_n;
   float plim;      // FP32 screening valid while max|p| <= plim * (smallest contact axis)
@@ -88,7 +91,9 @@ struct ConstOff {
   }
 };
 
-__host__ __device__ constexpr int nxi_pad(int nxi) { return (nxi + 1) & ~1; }
+// shared-memory row stride of xi / lambda: even (16-B aligned rows for LDS.128) and an odd
+// number of 16-B units, so 8 lanes loading 8 different rows hit 8 different bank groups
+__host__ __device__ constexpr int nxi_pad(int nxi) { return ((nxi + 1) & ~1) % 4 == 0 ? ((nxi + 1) & ~1) + 2 : ((nxi + 1) & ~1); }
 
 __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
 
@@ -150,6 +155,10 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
 #define SFB_TSUB(ph) do { } while (0)
 #endif
 
+#ifndef SFB_GREG
+#define SFB_GREG 1   // n <= 32: G partials in registers (1) or per-lane shared-memory slots (0)
+#endif
+
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
 template <int ND, int NXI, int NJ, bool BIG>
 __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {
@@ -159,7 +168,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
 
-  const int b = blockIdx.x;
+  // a member is owned by a cluster of csize CTAs; CTA rank crank owns a contiguous slice
+  // of the k-group tasks and all ranks run the (identical) KKT step redundantly
+  const int csize = P.csize;
+  const int crank = csize > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int b = blockIdx.x / csize;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = P.nw, nt = nw * 32;
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
@@ -337,6 +350,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   const bool robot_ok = i < n;
   const int ic = robot_ok ? i : n - 1;
   const int NTS = (NKG + SUB - 1) / SUB;
+  const int ts_lo = (NTS * crank) / csize, ts_hi = (NTS * (crank + 1)) / csize;
   const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
 
 #ifdef SFB_PHASE_TIMING
@@ -349,13 +363,14 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 
   for (int it = 0;; ++it) {
     // -------------------------------------------- A/B/C per k-group task
-    double Gp[BIG ? ND : 1][BIG ? NXI : 1];
+    constexpr bool GREG = BIG || SFB_GREG;   // partials held in registers
+    double Gp[GREG ? ND : 1][GREG ? NXI : 1];
     double* gl = sGl + (size_t)warp * NXI * ND * 32 + lane;          // this lane's partials, stride 32
-    if (BIG) {
+    if (GREG) {
 #pragma unroll
-      for (int a = 0; a < (BIG ? ND : 1); ++a)
+      for (int a = 0; a < (GREG ? ND : 1); ++a)
 #pragma unroll
-        for (int c = 0; c < (BIG ? NXI : 1); ++c) Gp[a][c] = 0.0;
+        for (int c = 0; c < (GREG ? NXI : 1); ++c) Gp[a][c] = 0.0;
     } else {
 #pragma unroll
       for (int q = 0; q < NXI * ND; ++q) gl[q * 32] = 0.0;
@@ -363,7 +378,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     float* posw = sPos + (size_t)(warp * SUB + sub) * NJ * ND2;        // !BIG: this k-group's row
     double s1 = 0.0, s2 = 0.0;
 
-    for (int ts = wk; ts < NTS; ts += nwk) {
+    for (int ts = ts_lo + wk; ts < ts_hi; ts += nwk) {
       const int kg_raw = ts * SUB + sub;
       const bool kg_ok = kg_raw < NKG;
       const int kg = kg_ok ? kg_raw : NKG - 1;
@@ -651,8 +666,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           const double2 w = wk2[c];
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
-            if (BIG) {
-              Gp[BIG ? a : 0][BIG ? c : 0] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[BIG ? a : 0][BIG ? c : 0]));
+            if (GREG) {
+              Gp[GREG ? a : 0][GREG ? c : 0] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[GREG ? a : 0][GREG ? c : 0]));
             } else {
               double* q = gl + (c * ND + a) * 32;
               *q = fma(w.x, g[a][0], fma(w.y, g[a][1], *q));
@@ -665,6 +680,12 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
 
     // -------------------------------------------- reductions
+    if (!BIG && GREG) {
+#pragma unroll
+      for (int a = 0; a < (GREG ? ND : 1); ++a)
+#pragma unroll
+        for (int c = 0; c < (GREG ? NXI : 1); ++c) gl[(c * ND + a) * 32] = Gp[a][c];
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       s1 += __shfl_xor_sync(FULL, s1, off);
@@ -703,7 +724,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #pragma unroll
         for (int a = 0; a < (BIG ? ND : 1); ++a)
 #pragma unroll
-          for (int c = 0; c < (BIG ? NXI : 1); ++c) dst[(a * 32 + lane) * NXI + c] = Gp[a][c];
+          for (int c = 0; c < (BIG ? NXI : 1); ++c) dst[(a * 32 + lane) * NXI + c] = Gp[BIG ? a : 0][BIG ? c : 0];
       }
       __syncthreads();
       for (int o = tid; o < nv; o += nt) {
@@ -729,10 +750,34 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       S2 += sRed[w * 4 + 1];
       FP += sRed[w * 4 + 3];
     }
+    if (csize > 1) {
+      // all-gather of the CTA partials (G, S1, S2) over DSMEM, summed in rank order by every
+      // CTA; buffers alternate by iteration so one cluster barrier per iteration suffices
+      auto cluster = cooperative_groups::this_cluster();
+      double* xg = reinterpret_cast<double*>(smem + P.L.xg) + (size_t)(it & 1) * (nv + 2);
+      for (int o = tid; o < nv; o += nt) xg[o] = sG[o];
+      if (tid == 0) {
+        xg[nv] = S1;
+        xg[nv + 1] = S2;
+      }
+      cluster.sync();
+      for (int o = tid; o < nv; o += nt) {
+        double acc = 0.0;
+        for (int r = 0; r < csize; ++r) acc += cluster.map_shared_rank(xg, r)[o];
+        sG[o] = acc;
+      }
+      S1 = S2 = 0.0;
+      for (int r = 0; r < csize; ++r) {
+        const double* rx = cluster.map_shared_rank(xg, r);
+        S1 += rx[nv];
+        S2 += rx[nv + 1];
+      }
+      __syncthreads();
+    }
     const double primal = sqrt(S1) + sqrt(S2);
     if (it > 0) last_fp = FP;
     ++c_evals;
-    if (tid == 0 && P.trace) {
+    if (tid == 0 && crank == 0 && P.trace) {
       double* tr = P.trace + ((size_t)b * (P.max_iters + 1) + it) * 2;
       tr[0] = primal;
       tr[1] = last_fp;
@@ -760,12 +805,12 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       }
       double* xo = P.xi + (size_t)b * nv;
       double* lo = P.lam + (size_t)b * nv;
-      for (int o = tid; o < nv; o += nt) {
+      for (int o = tid; crank == 0 && o < nv; o += nt) {
         const int ai = o / NXI, c = o - ai * NXI;
         xo[o] = sXi[ai * NXP + c];
         lo[o] = sLam[ai * NXP + c];
       }
-      if (tid == 0) {
+      if (tid == 0 && crank == 0) {
         P.primal[b] = primal;
         P.eq_max[b] = eq_max;
         P.iterations[b] = it;
@@ -898,7 +943,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       atomicAdd(cb + 0, c_exact);
       atomicAdd(cb + 1, c_active);
       atomicAdd(cb + 2, c_screen);
-      if (warp == 0) atomicAdd(cb + 3, c_evals);
+      if (warp == 0 && crank == 0) atomicAdd(cb + 3, c_evals);
     }
   }
 }

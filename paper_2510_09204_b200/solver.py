@@ -294,7 +294,7 @@ class DeviceBatch:
 
     def __init__(self, systems, xi0, lam0=None, target=None, kind="projection", cfg=None,
                  member_instance=None, early_exit=True, trace=True, counters=False,
-                 device=None):
+                 device=None, cluster=0):
         import torch
         cfg = cfg or SolverConfig()
         if not isinstance(systems, (list, tuple)):
@@ -352,6 +352,7 @@ class DeviceBatch:
             raise ShapeError("all instances of a batch must share d_max")
         self.d_max = d_max.pop()
         self.early_exit = bool(early_exit)
+        self.cluster = int(cluster)
         T = cfg.max_iters + 1
         self.out_xi = torch.empty_like(self.xi0)
         self.out_lam = torch.empty_like(self.xi0)
@@ -371,7 +372,8 @@ class DeviceBatch:
                                  _lib.BATCH_STATIC_OBSTACLES if self.obs_static else 0)
         c = self.cfg
         self._cfg = _lib.Config(float(c.rho), float(c.primal_tol), float(c.fp_tol),
-                                float(self.d_max), int(c.max_iters), 1 if self.early_exit else 0)
+                                float(self.d_max), int(c.max_iters), 1 if self.early_exit else 0,
+                                self.cluster)
         self._out = _lib.Out(p(self.out_xi), p(self.out_lam), p(self.out_primal), p(self.out_eq),
                              p(self.out_its), p(self.out_status), p(self.out_trace),
                              p(self.out_counters))
@@ -505,18 +507,21 @@ class BatchResult:
 
 def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projection",
                     cfg: SolverConfig | None = None, member_instance=None,
-                    fixed_iterations: bool = False, trace: bool = True) -> BatchResult:
+                    fixed_iterations: bool = False, trace: bool = True,
+                    cluster: int = 0) -> BatchResult:
     """Solve instances x samples in one launch (host arrays in, host arrays out).
 
     xi0/lam0/target: (B, n_d, n, n_basis) (numpy or torch, host or device);
     `systems[member_instance[b]]` is member b's constraint system. With
     fixed_iterations=True every member runs exactly cfg.max_iters + 1 map
-    evaluations (the throughput protocol of SURVEY.md §8(d))."""
+    evaluations (the throughput protocol of SURVEY.md §8(d)). `cluster` = CTAs per
+    member (0: auto — batches too small to fill the GPU split each member over a
+    thread-block cluster for latency)."""
     cfg = cfg or SolverConfig()
     t0 = time.perf_counter()
     batch = DeviceBatch(systems, xi0, lam0, target, kind=kind, cfg=cfg,
                         member_instance=member_instance, early_exit=not fixed_iterations,
-                        trace=trace)
+                        trace=trace, cluster=cluster)
     batch.launch()
     out = batch.results()
     return BatchResult(xi=out["xi"], lam=out["lam"], status=out["status"],
