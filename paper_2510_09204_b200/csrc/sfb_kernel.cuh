@@ -100,6 +100,14 @@ __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fa
 // append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
 __device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __funnelshift_l(t, m, 1); }
 
+// 1/sqrt(q) in FP64 from the FP32 MUFU seed and one Newton step (relative error ~1e-14,
+// vs ~1e-16 for rsqrt(double); the seed needs q inside the FP32 normal range)
+__device__ __forceinline__ double rsqrt_fast(double q) {
+  if (!(q > 1e-30 && q < 1e30)) return rsqrt(q);
+  const double y = (double)rsqrtf((float)q);
+  return y * fma(-0.5 * q, y * y, 1.5);
+}
+
 // Exact FP64 residual of one separation row (constraints.py:166-247, trig-free):
 // r1 = delta * (1 - clip(rho, 1, d_max) / rho), coincident rows use alpha = 0, beta = pi/2.
 template <int ND>
@@ -116,7 +124,7 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
       if (ND == 3) r[ND - 1] = -ax_b * COS_HALF_PI * coinc_sign;
       return true;
     }
-    f = 1.0 - rsqrt(q);
+    f = 1.0 - rsqrt_fast(q);
   } else if (q > d_max * d_max) {
     f = 1.0 - d_max * rsqrt(q);
   } else {
@@ -156,7 +164,7 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
 #endif
 
 #ifndef SFB_GREG
-#define SFB_GREG 1   // n <= 32: G partials in registers (1) or per-lane shared-memory slots (0)
+#define SFB_GREG 0   // n <= 32: G partials in registers (1) or per-lane shared-memory slots (0)
 #endif
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
@@ -354,7 +362,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
 
 #ifdef SFB_PHASE_TIMING
-  long long t_ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_ph[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t_last = clock64(), t_sub = t_last;
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
@@ -568,8 +576,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           if (P.obs_static) {
             // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
             const float* ob = sObsS + (size_t)o0 * OS;
-#pragma unroll 4
-            for (int o = 0; o < oc; ++o) {
+            for (int o4 = 0; o4 < oc; o4 += 4)   // MP is a multiple of 4
+#pragma unroll
+            for (int o = o4; o < o4 + 4; ++o) {
               const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
               const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
               const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
@@ -706,12 +715,15 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         const int ii = o & 31, col = o >> 5;
         if (ii >= n) continue;
         const int c = col / ND, a = col - c * ND;
-        double acc = 0.0;
-        for (int w = 0; w < nw; ++w) {
-          const double* src = sGl + (size_t)(w * NXI * ND + col) * 32 + ii;
+        double v[NW * SUB];
 #pragma unroll
-          for (int s2i = 0; s2i < SUB; ++s2i) acc += src[s2i * NJ];
-        }
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int s2i = 0; s2i < SUB; ++s2i)
+            v[w * SUB + s2i] = w < nw ? sGl[(size_t)(w * NXI * ND + col) * 32 + ii + s2i * NJ] : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW * SUB; ++q) acc += v[q];
         sG[(a * n + ii) * NXI + c] = acc;
       }
       __syncthreads();
@@ -751,28 +763,49 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       FP += sRed[w * 4 + 3];
     }
     if (csize > 1) {
-      // all-gather of the CTA partials (G, S1, S2) over DSMEM, summed in rank order by every
-      // CTA; buffers alternate by iteration so one cluster barrier per iteration suffices
+      // Cluster reduction of the CTA partials (G and S1, S2) in two pushes over DSMEM:
+      //  1. reduce-scatter: the partial slice s goes to rank s (remote stores),
+      //  2. rank s sums its slice over the ranks in rank order and stores the result into
+      //     every rank's final buffer.
+      // Buffers alternate by iteration parity (each is reused only after two more barriers).
       auto cluster = cooperative_groups::this_cluster();
-      double* xg = reinterpret_cast<double*>(smem + P.L.xg) + (size_t)(it & 1) * (nv + 2);
-      for (int o = tid; o < nv; o += nt) xg[o] = sG[o];
+      const int tot = nv + 2, SL = (tot + csize - 1) / csize;
+      double* xg = reinterpret_cast<double*>(smem + P.L.xg);
+      double* recv = xg + (size_t)(it & 1) * (8 * SL + tot);     // [csize][SL]
+      double* fin = recv + 8 * SL;                                // [tot]
       if (tid == 0) {
-        xg[nv] = S1;
-        xg[nv + 1] = S2;
-      }
-      cluster.sync();
-      for (int o = tid; o < nv; o += nt) {
-        double acc = 0.0;
-        for (int r = 0; r < csize; ++r) acc += cluster.map_shared_rank(xg, r)[o];
-        sG[o] = acc;
-      }
-      S1 = S2 = 0.0;
-      for (int r = 0; r < csize; ++r) {
-        const double* rx = cluster.map_shared_rank(xg, r);
-        S1 += rx[nv];
-        S2 += rx[nv + 1];
+        sG[nv] = S1;
+        sG[nv + 1] = S2;
       }
       __syncthreads();
+#ifdef SFB_PHASE_TIMING
+      if (tid == 0) t_sub = clock64();
+#endif
+      for (int o = tid; o < tot; o += nt) {
+        const int sr = o / SL;
+        cluster.map_shared_rank(recv, sr)[crank * SL + (o - sr * SL)] = sG[o];
+      }
+      cluster.sync();
+      SFB_TSUB(11);
+      double* fr[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) fr[r] = cluster.map_shared_rank(fin, r < csize ? r : 0);
+      for (int j = tid; j < SL; j += nt) {
+        const int o = crank * SL + j;
+        if (o >= tot) break;
+        double acc = 0.0;
+        for (int r = 0; r < csize; ++r) acc += recv[r * SL + j];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < csize) fr[r][o] = acc;
+      }
+      cluster.sync();
+      SFB_TSUB(12);
+      for (int o = tid; o < tot; o += nt) sG[o] = fin[o];
+      __syncthreads();
+      S1 = sG[nv];
+      S2 = sG[nv + 1];
+      SFB_TSUB(13);
     }
     const double primal = sqrt(S1) + sqrt(S2);
     if (it > 0) last_fp = FP;
@@ -889,10 +922,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp
     for (int col = warp; col < ncolD; col += nw) {
       const int a = col / NXI, c = col - a * NXI;
-      double mean = 0.0;
+      double m0 = 0.0, m1 = 0.0;
 #pragma unroll
-      for (int c2 = 0; c2 < NXI; ++c2) mean = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], mean);
-      for (int r = 0; r < NB; ++r) mean = fma(sDxb[c * NB + r], sSU[a * NB + r], mean);
+      for (int c2 = 0; c2 < NXI; ++c2) m0 = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], m0);
+      for (int r = 0; r < NB; ++r) m1 = fma(sDxb[c * NB + r], sSU[a * NB + r], m1);
+      const double mean = m0 + m1;
       for (int i0 = 0; i0 < n; i0 += 32) {
         const int ii = i0 + lane;
         if (ii < n) {
@@ -923,7 +957,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   }
 #ifdef SFB_PHASE_TIMING
   if (tid == 0 && P.counters) {
-    for (int q = 0; q < 11; ++q) P.counters[(size_t)b * 16 + 4 + q] = (unsigned long long)t_ph[q];
+    for (int q = 0; q < 14; ++q) P.counters[(size_t)b * 20 + 4 + q] = (unsigned long long)t_ph[q];
   }
 #endif
 
@@ -936,7 +970,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
     if (lane == 0) {
 #ifdef SFB_PHASE_TIMING
-      unsigned long long* cb = P.counters + (size_t)b * 16;
+      unsigned long long* cb = P.counters + (size_t)b * 20;
 #else
       unsigned long long* cb = P.counters + (size_t)b * 4;
 #endif

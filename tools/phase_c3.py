@@ -9,17 +9,23 @@ from paper_2510_09204_b200 import solver
 
 systems, xi, mi = bench.make_workload(0)
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 500
+n_inst = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+cluster = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+sel = mi < n_inst
+systems, xi, mi = systems[:n_inst], xi[sel], mi[sel]
 batch = solver.DeviceBatch(systems, xi, None, xi, cfg=solver.SolverConfig(max_iters=L),
-                           member_instance=mi, early_exit=False, trace=False, counters=True)
-batch.out_counters = torch.zeros((batch.B, 16), dtype=torch.int64, device=batch.device)
+                           member_instance=mi, early_exit=False, trace=False, counters=True,
+                           cluster=cluster)
+batch.out_counters = torch.zeros((batch.B, 20), dtype=torch.int64, device=batch.device)
 batch._build_structs()
 batch.launch(); torch.cuda.synchronize()
 batch.launch(); torch.cuda.synchronize()
 c = batch.out_counters.cpu().numpy().astype(float)
 names = ["tasks", "bar_after_tasks", "G_reduce", "decision", "K1+bar", "K2+K3+bar"]
-sub_names = ["  positions", "  robot screen", "  robot exact", "  obstacles", "  box+contract"]
+sub_names = ["  positions", "  robot screen", "  robot exact", "  obstacles", "  box+contract",
+             "  cluster.sync", "  dsmem reads", "  post-read bar"]
 per = c[:, 4:10].mean(axis=0) / (L + 1)
-sub = c[:, 10:15].mean(axis=0) / (L + 1)
+sub = c[:, 10:18].mean(axis=0) / (L + 1)
 tot = per.sum()
 for nm, v in zip(names, per):
     print(f"{nm:18s} {v:9.0f} cycles/iter ({v / tot * 100:5.1f}%)")
