@@ -159,6 +159,22 @@ def _dense_kkt_cond(sys, kind: str, rho: float) -> float:
     return float(np.linalg.cond(M))
 
 
+_A_OK: dict = {}
+
+
+def _kron_checked(A: np.ndarray, n: int, E: np.ndarray) -> bool:
+    """A == I_n (x) E, memoised on the identity and contents fingerprint of A."""
+    key = (id(A), A.__array_interface__["data"][0], A.shape, float(A.sum()), float(np.abs(A).sum()))
+    hit = _A_OK.get(key)
+    if hit is not None:
+        return hit
+    ok = bool(np.array_equal(A, np.kron(np.eye(n), E)))
+    if len(_A_OK) > 4096:
+        _A_OK.clear()
+    _A_OK[key] = ok
+    return ok
+
+
 def system_data(sys, kind: str = "projection", rho: float = 1.0) -> SystemData:
     """Extract and validate the structured data of a (reference or local) ConstraintSystem."""
     d = sys.dims
@@ -170,7 +186,7 @@ def system_data(sys, kind: str = "projection", rho: float = 1.0) -> SystemData:
         raise UsageError("boundary matrix A is not I_n (x) E: unsupported constraint system")
     nb = A.shape[0] // n
     E = A[:nb, :n_xi].copy()
-    if not np.array_equal(A, np.kron(np.eye(n), E)):
+    if not _kron_checked(A, n, E):
         if _dense_kkt_cond(sys, kind, rho) > 1e14:
             raise SetupError("KKT matrix is singular or near-singular")
         raise UsageError("boundary matrix A is not I_n (x) E: unsupported constraint system")
@@ -285,6 +301,23 @@ def _as_tensor(x, device, dtype, counter=None):
     return t.to(device)
 
 
+_PINNED = {"buf": None}
+
+
+def _pinned(n: int):
+    """Grow-only pinned host staging buffer (float64) for the input arena."""
+    import torch
+    buf = _PINNED["buf"]
+    if buf is None or buf.numel() < n:
+        size = max(n, 1 << 16)
+        try:
+            buf = torch.empty(size, dtype=torch.float64).pin_memory()
+        except RuntimeError:                      # no CUDA context yet / no pinning available
+            buf = torch.empty(size, dtype=torch.float64)
+        _PINNED["buf"] = buf
+    return buf
+
+
 class DeviceBatch:
     """A batch of members (instance x sample) resident on one GPU.
 
@@ -313,23 +346,32 @@ class DeviceBatch:
         self.kind, self.cfg = kind, cfg
         n, n_d, n_xi = sd0.n, sd0.n_d, sd0.n_basis
         f64, dev = torch.float64, self.device
-        h2d = [0]
-        self.xi0 = _as_tensor(xi0, dev, f64, h2d)
-        B = self.xi0.shape[0]
-        if tuple(self.xi0.shape) != (B, n_d, n, n_xi):
-            raise ShapeError(f"xi0 has shape {tuple(self.xi0.shape)}, expected (B, {n_d}, {n}, {n_xi})")
+        # ---- inputs: host arrays are packed into one buffer and cross PCIe in one copy;
+        # CUDA tensors (e.g. straight from a PyTorch sampler) are used in place
+        host_parts, dev_parts = [], {}
+
+        def add(name, x, shape, dtype=np.float64):
+            if isinstance(x, torch.Tensor) and x.is_cuda:
+                t = x.to(device=dev, dtype=torch.float64 if dtype == np.float64 else torch.int32)
+                dev_parts[name] = t.contiguous()
+                return tuple(t.shape)
+            a = x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x
+            a = np.ascontiguousarray(np.asarray(a, dtype=dtype))
+            host_parts.append((name, a))
+            return a.shape
+
+        xshape = add("xi0", xi0, None)
+        B = xshape[0]
+        if tuple(xshape) != (B, n_d, n, n_xi):
+            raise ShapeError(f"xi0 has shape {tuple(xshape)}, expected (B, {n_d}, {n}, {n_xi})")
         self.B = B
-        self.lam0 = (torch.zeros_like(self.xi0) if lam0 is None else _as_tensor(lam0, dev, f64, h2d))
-        if tuple(self.lam0.shape) != tuple(self.xi0.shape):
+        if lam0 is not None and add("lam0", lam0, None) != xshape:
             raise ShapeError("lam0 shape differs from xi0")
         if kind == "projection":
             if target is None:
                 raise ShapeError("projection mode needs a target")
-            self.target = _as_tensor(target, dev, f64, h2d)
-            if tuple(self.target.shape) != tuple(self.xi0.shape):
+            if add("target", target, None) != xshape:
                 raise ShapeError("target shape differs from xi0")
-        else:
-            self.target = None
         if member_instance is None:
             if len(sds) != 1 and len(sds) != B:
                 raise ShapeError("member_instance is required when instances != members")
@@ -337,30 +379,68 @@ class DeviceBatch:
         mi = np.asarray(member_instance, np.int32)
         if mi.shape != (B,) or mi.min(initial=0) < 0 or mi.max(initial=0) >= len(sds):
             raise ShapeError("member_instance out of range")
-        self.member_instance = _as_tensor(mi, dev, torch.int32, h2d)
-        self.bvals = _as_tensor(np.stack([s.bvals for s in sds]), dev, f64, h2d)
-        self.box = _as_tensor(np.stack([s.box for s in sds]), dev, f64, h2d)
-        obs_np = np.stack([s.obs_pos for s in sds])
+        add("bvals", np.stack([q.bvals for q in sds]), None)
+        add("box", np.stack([q.box for q in sds]), None)
+        obs_np = np.stack([q.obs_pos for q in sds])
         self.obs_static = bool(obs_np.size == 0 or np.all(obs_np == obs_np[..., :1]))
-        self.obs_pos = _as_tensor(obs_np, dev, f64, h2d)
-        self.obs_axes = _as_tensor(np.stack([s.obs_axes for s in sds]), dev, f64, h2d)
-        self.pair_axes = _as_tensor(np.stack([s.pair_axes for s in sds]), dev, f64, h2d)
-        self.h2d_bytes = h2d[0]
+        add("obs_pos", obs_np, None)
+        add("obs_axes", np.stack([q.obs_axes for q in sds]), None)
+        add("pair_axes", np.stack([q.pair_axes for q in sds]), None)
+        # member_instance rides in the float64 arena as raw int32 words
+        mi_words = np.zeros((B + 1) // 2 * 2, np.int32)
+        mi_words[:B] = mi
+        host_parts.append(("member_instance", mi_words.view(np.float64)))
+        offs, total = {}, 0
+        for name, a in host_parts:
+            offs[name] = (total, a.shape)
+            total += a.size
+        staging = _pinned(total)
+        arena_h = staging.numpy()[:total]
+        for name, a in host_parts:
+            o, _ = offs[name]
+            arena_h[o: o + a.size] = a.reshape(-1)
+        self._in_arena = staging[:total].to(dev)       # synchronous copy from pinned memory
+        self.h2d_bytes = int(arena_h.nbytes)
+        views = {}
+        for name, (o, shp) in offs.items():
+            views[name] = self._in_arena[o: o + int(np.prod(shp))].view(shp)
+        views.update(dev_parts)
+        self.xi0 = views["xi0"]
+        self.lam0 = views.get("lam0")
+        if self.lam0 is None:
+            self.lam0 = torch.zeros_like(self.xi0)
+        self.target = views.get("target") if kind == "projection" else None
+        self.member_instance = views["member_instance"].view(torch.int32)[:B]
+        self.bvals, self.box = views["bvals"], views["box"]
+        self.obs_pos, self.obs_axes, self.pair_axes = views["obs_pos"], views["obs_axes"], views["pair_axes"]
         self.n_instances = len(sds)
-        d_max = {s.d_max for s in sds}
+        d_max = {q.d_max for q in sds}
         if len(d_max) != 1:
             raise ShapeError("all instances of a batch must share d_max")
         self.d_max = d_max.pop()
         self.early_exit = bool(early_exit)
         self.cluster = int(cluster)
+        # ---- outputs: one arena, one device-to-host copy
         T = cfg.max_iters + 1
-        self.out_xi = torch.empty_like(self.xi0)
-        self.out_lam = torch.empty_like(self.xi0)
-        self.out_primal = torch.empty(B, dtype=f64, device=dev)
-        self.out_eq = torch.empty(B, dtype=f64, device=dev)
-        self.out_its = torch.empty(B, dtype=torch.int32, device=dev)
-        self.out_status = torch.empty(B, dtype=torch.int32, device=dev)
-        self.out_trace = torch.empty((B, T, 2), dtype=f64, device=dev) if trace else None
+        nvm = B * n_d * n * n_xi
+        seg = [("xi", nvm), ("lam", nvm), ("primal", B), ("eq", B), ("its", (B + 1) // 2),
+               ("status", (B + 1) // 2)]
+        if trace:
+            seg.append(("trace", B * T * 2))
+        oofs, ototal = {}, 0
+        for name, sz in seg:
+            oofs[name] = (ototal, sz)
+            ototal += sz
+        self._out_arena = torch.empty(ototal, dtype=f64, device=dev)
+        ov = {k: self._out_arena[o: o + sz] for k, (o, sz) in oofs.items()}
+        self.out_xi = ov["xi"].view(B, n_d, n, n_xi)
+        self.out_lam = ov["lam"].view(B, n_d, n, n_xi)
+        self.out_primal, self.out_eq = ov["primal"], ov["eq"]
+        self.out_its = ov["its"].view(torch.int32)[:B]
+        self.out_status = ov["status"].view(torch.int32)[:B]
+        self.out_trace = ov["trace"].view(B, T, 2) if trace else None
+        self._out_prefix = oofs["status"][0] + oofs["status"][1]   # everything but the trace
+        self._oofs = oofs
         self.out_counters = torch.zeros((B, 4), dtype=torch.int64, device=dev) if counters else None
         self._build_structs()
 
@@ -387,20 +467,26 @@ class DeviceBatch:
         _lib.check(rc, "sfb_solve")
 
     def results(self) -> dict:
-        """Copy results to the host (synchronizes). Member-major arrays."""
-        its = self.out_its.cpu().numpy()
-        d2h = its.nbytes + sum(t.numel() * t.element_size() for t in
-                               (self.out_xi, self.out_lam, self.out_primal, self.out_eq, self.out_status))
+        """Copy results to the host (synchronizes): one copy of the output arena (the trace
+        only up to the longest member's iterations). Member-major arrays."""
+        import torch
+        B, n_d, n, n_xi = self.out_xi.shape
+        head = self._out_arena[: self._out_prefix].cpu().numpy()
+        o = self._oofs
+        get = lambda k: head[o[k][0]: o[k][0] + o[k][1]]
+        its = get("its").view(np.int32)[:B].copy()
+        st = get("status").view(np.int32)[:B]
         out = {
-            "xi": self.out_xi.cpu().numpy(), "lam": self.out_lam.cpu().numpy(),
-            "primal": self.out_primal.cpu().numpy(), "eq_max": self.out_eq.cpu().numpy(),
-            "iterations": its, "status": [_lib.STATUS[int(s)] for s in self.out_status.cpu().numpy()],
+            "xi": get("xi").reshape(B, n_d, n, n_xi).copy(), "lam": get("lam").reshape(B, n_d, n, n_xi).copy(),
+            "primal": get("primal").copy(), "eq_max": get("eq").copy(),
+            "iterations": its, "status": [_lib.STATUS[int(v)] for v in st],
         }
+        d2h = head.nbytes
         if self.out_trace is not None:
             T = int(its.max()) + 1 if its.size else 0
             tr = self.out_trace[:, :T].cpu().numpy()
             d2h += tr.nbytes
-            out["trace"] = [tr[b, : its[b] + 1] for b in range(self.B)]
+            out["trace"] = [tr[b, : its[b] + 1] for b in range(B)]
         if self.out_counters is not None:
             out["counters"] = self.out_counters.cpu().numpy()
         out["d2h_bytes"] = d2h
