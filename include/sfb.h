@@ -117,6 +117,13 @@ typedef struct sfb_out {
 int sfb_solve(const sfb_plan* plan, const sfb_batch* batch, const sfb_config* cfg,
               const sfb_out* out, void* stream);
 
+/* Post-solve epilogue of the reference's time scaling (basis.py:119-142): per member, the
+ * largest speed and acceleration norm over robots and the dense grid rows of Wd / Wdd
+ * ([k_dense][n_basis], FP64). coeffs [B][n_d][n][n_basis]; all pointers on the device. */
+int sfb_kinematic_peaks(const double* coeffs, int32_t n_members, int32_t n_d, int32_t n,
+                        int32_t n_basis, const double* Wd, const double* Wdd, int32_t k_dense,
+                        double* vmax, double* amax, void* stream);
+
 /* Dynamic shared memory one member needs (0 if the shape is unsupported). */
 int64_t sfb_smem_bytes(const sfb_plan* plan);
 

@@ -10,7 +10,9 @@ from .problem import (BasisConfig, BasisMatrices, ConstraintSystem, Obstacle, Sc
                       ScenarioFamily, SystemDims, assemble, build_basis, generate,
                       sample_naive_prior, stack_xi, straight_line_coeffs, xi_from_coeffs)
 from .solver import (BatchResult, DeviceBatch, KktCache, ObjectiveMode, SolverConfig,
-                     SolverResult, SolverState, cold_start, fixed_point_step, solve,
-                     solve_batch, solve_instances, state_from_xi)
+                     SolverResult, SolverState, batch_primal_residual, cold_start,
+                     fixed_point_step, kinematic_peaks, primal_residual, rank_candidates,
+                     solve, solve_batch, solve_instances, state_from_xi, time_scale_batch,
+                     time_scale_for_limits)
 
 __version__ = "0.1.0"

@@ -16,7 +16,7 @@ SFB_OK, SFB_EINVAL, SFB_ESETUP, SFB_ECUDA, SFB_ENOMEM = 0, 1, 2, 3, 4
 MODE = {"projection": 0, "smoothness": 1}
 STATUS = {0: "max_iters", 1: "converged_primal", 2: "converged_fp"}
 EXPORTS = ("sfb_plan_create", "sfb_plan_destroy", "sfb_plan_cond", "sfb_solve",
-           "sfb_smem_bytes", "sfb_last_error", "sfb_abi_version")
+           "sfb_smem_bytes", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks")
 
 
 class Dims(ctypes.Structure):
@@ -80,6 +80,9 @@ def lib() -> ctypes.CDLL:
     L.sfb_smem_bytes.restype = ctypes.c_int64
     L.sfb_solve.argtypes = [vp, ctypes.POINTER(Batch), ctypes.POINTER(Config), ctypes.POINTER(Out), vp]
     L.sfb_solve.restype = ctypes.c_int
+    L.sfb_kinematic_peaks.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, vp, vp, ctypes.c_int32, vp, vp, vp]
+    L.sfb_kinematic_peaks.restype = ctypes.c_int
     L.sfb_last_error.argtypes = []
     L.sfb_last_error.restype = ctypes.c_char_p
     L.sfb_abi_version.argtypes = []

@@ -630,3 +630,76 @@ def state_from_xi(xi: np.ndarray, lam: np.ndarray | None = None) -> SolverState:
         xi = xi[:, :, None]
     lam = np.zeros_like(xi) if lam is None else (lam[:, :, None] if lam.ndim == 2 else lam)
     return SolverState(xi=xi.astype(float), lam=lam.astype(float))
+
+
+# ------------------------------------------------ callers either side of the solve
+
+
+def batch_primal_residual(xi, sys) -> np.ndarray:
+    """solver.py:185-187: primal residual of every member of xi (n_d, nv, B), on the GPU
+    (the map's analysis half only: a zero-iteration solve). The planner ranks its
+    candidates by this value (pipeline.py:113-115)."""
+    xi = np.asarray(xi, float)
+    if xi.ndim == 2:
+        xi = xi[:, :, None]
+    d = sys.dims
+    mm = to_member_major(xi, d.n, d.n_basis)
+    cfg = SolverConfig(max_iters=0, d_max=float(sys.d_max))
+    out = solve_instances([sys], mm, None, mm, cfg=cfg, fixed_iterations=True, trace=False)
+    return np.asarray(out.primal, float)
+
+
+def primal_residual(state: SolverState, sys):
+    """solver.py:177-182."""
+    out = batch_primal_residual(state.xi, sys)
+    return float(out[0]) if out.size == 1 else out
+
+
+def rank_candidates(xi_all, sys) -> tuple[np.ndarray, np.ndarray]:
+    """Stage 1 of pipeline.plan (pipeline.py:113-115): residuals and the stable order."""
+    pre = batch_primal_residual(xi_all, sys)
+    return pre, np.argsort(pre, kind="stable")
+
+
+def kinematic_peaks(xi_mm, basis, dense_factor: int = 10):
+    """Largest speed / acceleration norm per member over robots and the dense grid of
+    time_scale_for_limits (basis.py:134-139), computed on the GPU.
+    xi_mm: (B, n_d, n, n_basis) member-major coefficients (numpy or CUDA tensor)."""
+    import torch
+    from .problem import BasisConfig, build_basis
+    cfg = basis.config
+    dense = build_basis(BasisConfig(cfg.n_basis, dense_factor * (cfg.num_steps - 1) + 1, cfg.duration))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = xi_mm if isinstance(xi_mm, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(xi_mm, float))
+    x = x.to(device=dev, dtype=torch.float64).contiguous()
+    B, n_d, n, n_xi = x.shape
+    wd = torch.from_numpy(np.ascontiguousarray(dense.Wd)).to(dev)
+    wdd = torch.from_numpy(np.ascontiguousarray(dense.Wdd)).to(dev)
+    out = torch.empty((2, B), dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream(dev)
+    rc = _lib.lib().sfb_kinematic_peaks(x.data_ptr(), B, n_d, n, n_xi, wd.data_ptr(), wdd.data_ptr(),
+                                        dense.Wd.shape[0], out[0].data_ptr(), out[1].data_ptr(),
+                                        ctypes.c_void_p(s.cuda_stream))
+    _lib.check(rc, "sfb_kinematic_peaks")
+    o = out.cpu().numpy()
+    return o[0], o[1]
+
+
+def time_scale_batch(xi_mm, basis, v_max: float, a_max: float, dense_factor: int = 10) -> np.ndarray:
+    """gamma = max(1, vhat/v_max, sqrt(ahat/a_max)) per member (basis.py:119-142)."""
+    from .errors import ConfigError
+    if not (v_max > 0 and a_max > 0):
+        raise ConfigError("v_max and a_max must be positive")
+    vhat, ahat = kinematic_peaks(xi_mm, basis, dense_factor)
+    return np.maximum(1.0, np.maximum(vhat / v_max, np.sqrt(ahat / a_max)))
+
+
+def time_scale_for_limits(coeffs, basis, v_max: float, a_max: float, dense_factor: int = 10):
+    """basis.py:119-142 (single trajectory set (n, n_d, n_basis)): returns (gamma, basis
+    rebuilt with duration gamma*T)."""
+    from .problem import BasisConfig, build_basis
+    c = np.asarray(coeffs, float)
+    mm = c.transpose(1, 0, 2)[None]
+    gamma = float(time_scale_batch(mm, basis, v_max, a_max, dense_factor)[0])
+    cfg = basis.config
+    return gamma, build_basis(BasisConfig(cfg.n_basis, cfg.num_steps, gamma * cfg.duration))
