@@ -48,6 +48,7 @@ struct Layout {       // byte offsets into dynamic shared memory
 
 struct KParams {
   int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
+  int kgs;         // n > 32: k-group rows of positions held per CTA (its time slice)
   int csize;       // CTAs per member (thread-block cluster along the time axis), 1..8
   int mode, max_iters, early_exit;
   double rho, primal_tol, fp_tol, d_max, inv_n;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   // n > 32: positions of every k-group are shared by the robot-block warps of that k-group;
   // n <= 32: a warp holds all robots of its k-groups, so it owns a private position row
   float* sPos = reinterpret_cast<float*>(uni);                      // BIG [NKG][NROW][ND2] / [nw][32/NJ][NJ][ND2]
-  float* sLo = sPos + (size_t)NKG * NROW * ND2;                     // [NKG][NROW][ND2] lo (BIG)
+  float* sLo = sPos + (size_t)P.kgs * NROW * ND2;                   // [kgs][NROW][ND2] lo (BIG)
   double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots (BIG)
   // n <= 32: per-lane G partials [nw][NXI][ND][32] (conflict-free, lane-contiguous)
   double* sGl = reinterpret_cast<double*>(smem + P.L.gl);
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
         if (ND == 3) hv[6] = hv[7] = 0.f;
         if (BIG ? (kg_ok && robot_ok) : true) {
-          float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)kg * NROW + i) * ND2 : posw + i * ND2);
+          float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + i) * ND2 : posw + i * ND2);
           dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
           if (BIG) {
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
               lv[2 * a + 1] = has1 ? (float)(p[a][1] - (double)hv[2 * a + 1]) : 0.f;
             }
             if (ND == 3) lv[6] = lv[7] = 0.f;
-            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)kg * NROW + i) * ND2);
+            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)(kg - ts_lo) * NROW + i) * ND2);
             dl[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
             if (ND == 3) dl[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
           }
@@ -455,10 +456,10 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       }
       pabs = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(pabs)));
       if (BIG) {
-        if (lane == 0) sPmax[kg * 8 + rbk] = pabs;
+        if (lane == 0) sPmax[(kg - ts_lo) * 8 + rbk] = pabs;
         // every robot block of this k-group must have stored its positions
         asm volatile("bar.sync %0, %1;" ::"r"(1 + wk), "r"(P.RB * 32) : "memory");
-        for (int r = 0; r < P.RB; ++r) pabs = fmaxf(pabs, sPmax[kg * 8 + r]);
+        for (int r = 0; r < P.RB; ++r) pabs = fmaxf(pabs, sPmax[(kg - ts_lo) * 8 + r]);
       } else {
         __syncwarp();
       }
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         unsigned mask = 0u;
         if (!force) {
           const float2 thr2 = make_float2(-r_thr, -r_thr);
-          const float* base = BIG ? sPos + ((size_t)kg * NROW + j0) * ND2 : posw;
+          const float* base = BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + j0) * ND2 : posw;
           unsigned mm = 0u;
           auto screen = [&](const float* bp) {
             const float4 v = *reinterpret_cast<const float4*>(bp);
@@ -523,8 +524,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           const int j = j0 + jl;
           double pj[ND][2];
           if (BIG) {
-            const float* hp = sPos + ((size_t)kg * NROW + (act ? j : 0)) * ND2;
-            const float* lp = sLo + ((size_t)kg * NROW + (act ? j : 0)) * ND2;
+            const float* hp = sPos + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
+            const float* lp = sLo + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
 #pragma unroll
             for (int a = 0; a < ND; ++a)
 #pragma unroll
@@ -764,15 +765,14 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
     if (csize > 1) {
       // Cluster reduction of the CTA partials (G and S1, S2) in two pushes over DSMEM:
-      //  1. reduce-scatter: the partial slice s goes to rank s (remote stores),
-      //  2. rank s sums its slice over the ranks in rank order and stores the result into
-      //     every rank's final buffer.
-      // Buffers alternate by iteration parity (each is reused only after two more barriers).
+      //  1. reduce-scatter: the partial slice s goes to rank s's receive buffer,
+      //  2. rank s sums its slice over the ranks in rank order and stores the sum into every
+      //     rank's G (whose local partial was already scattered in step 1).
+      // A cluster barrier follows each push; the receive buffer of step t is read before
+      // barrier 2 of step t, so no buffer is rewritten while it can still be read.
       auto cluster = cooperative_groups::this_cluster();
       const int tot = nv + 2, SL = (tot + csize - 1) / csize;
-      double* xg = reinterpret_cast<double*>(smem + P.L.xg);
-      double* recv = xg + (size_t)(it & 1) * (8 * SL + tot);     // [csize][SL]
-      double* fin = recv + 8 * SL;                                // [tot]
+      double* recv = reinterpret_cast<double*>(smem + P.L.xg);   // [csize][SL]
       if (tid == 0) {
         sG[nv] = S1;
         sG[nv + 1] = S2;
@@ -787,9 +787,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       }
       cluster.sync();
       SFB_TSUB(11);
-      double* fr[8];
+      double* gr[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) fr[r] = cluster.map_shared_rank(fin, r < csize ? r : 0);
+      for (int r = 0; r < 8; ++r) gr[r] = cluster.map_shared_rank(sG, r < csize ? r : 0);
       for (int j = tid; j < SL; j += nt) {
         const int o = crank * SL + j;
         if (o >= tot) break;
@@ -797,12 +797,10 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         for (int r = 0; r < csize; ++r) acc += recv[r * SL + j];
 #pragma unroll
         for (int r = 0; r < 8; ++r)
-          if (r < csize) fr[r][o] = acc;
+          if (r < csize) gr[r][o] = acc;
       }
       cluster.sync();
       SFB_TSUB(12);
-      for (int o = tid; o < tot; o += nt) sG[o] = fin[o];
-      __syncthreads();
       S1 = sG[nv];
       S2 = sG[nv + 1];
       SFB_TSUB(13);

@@ -1,0 +1,91 @@
+"""Throughput of the SF kernel across the BASELINE.json configs (C1-C4) and the
+robots x batch sweep (C5: 8-128 robots, batch 1-1024 instances, 20 obstacles,
+box half-width max(1, 2 sqrt(n/32)), T=100, L=500). Device-timed
+(CUDA events, inputs resident), one GPU. Writes profiles/r01_sweep.json.
+
+    python tools/sweep.py [--quick]
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2510_09204_b200 import solver  # noqa: E402
+from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble, build_basis,  # noqa: E402
+                                           generate, sample_naive_prior, stack_xi)
+
+
+def workload(n, m, h, instances, samples, seed0):
+    basis = build_basis(BasisConfig(11, 100, 5.0))
+    fam = ScenarioFamily("random_box", robot_radius=0.1, box=(-h, h), n_obstacles=m)
+    systems, xs = [], []
+    uniq = min(instances, 64)   # distinct scenarios (generation is host-side and slow at n=128)
+    for i in range(uniq):
+        scn = generate(fam, n, 2, seed=seed0 + i, horizon=basis.config)
+        systems.append(assemble(scn, basis))
+        xs.append(solver.to_member_major(stack_xi(sample_naive_prior(scn, basis, samples, seed=seed0 + i)), n, 11))
+    reps = [i % uniq for i in range(instances)]
+    xi = np.concatenate([xs[r] for r in reps])
+    mi = np.repeat(np.arange(instances), samples).astype(np.int32)
+    return [systems[r] for r in reps], xi, mi
+
+
+def time_solve(systems, xi, mi, L, reps=3):
+    cfg = solver.SolverConfig(max_iters=L)
+    batch = solver.DeviceBatch(systems, xi, None, xi, cfg=cfg, member_instance=mi, early_exit=False,
+                               trace=False)
+    batch.launch()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ts = []
+    for _ in range(reps):
+        ev[0].record()
+        batch.launch()
+        ev[1].record()
+        torch.cuda.synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]) / 1e3)
+    return min(ts), batch.plan.smem_bytes
+
+
+def main():
+    quick = "--quick" in sys.argv
+    L = 500
+    rows = []
+    named = [("C1", 4, 0, 1.0, 1, 1), ("C2", 16, 10, 1.0, 32, 1), ("C3", 32, 20, 2.0, 64, 8),
+             ("C4", 64, 30, 2.0, 128, 1)]
+    for name, n, m, h, inst, samp in named:
+        systems, xi, mi = workload(n, m, h, inst, samp, 1000 * int(name[1]))
+        t, smem = time_solve(systems, xi, mi, L)
+        rows.append(dict(config=name, robots=n, obstacles=m, instances=inst, samples=samp,
+                         members=inst * samp, L=L, seconds=t, instances_per_s=inst / t,
+                         member_iters_per_s=inst * samp * (L + 1) / t, smem_bytes=smem))
+        print(json.dumps(rows[-1]), flush=True)
+    robots = [8, 16, 32, 64, 128]
+    batches = [1, 8, 64, 256, 1024] if not quick else [1, 64]
+    for n in robots:
+        h = max(1.0, 2.0 * math.sqrt(n / 32))
+        for inst in batches:
+            if n == 128 and inst > 256:
+                continue
+            systems, xi, mi = workload(n, 20, h, inst, 1, 5000 + n)
+            t, smem = time_solve(systems, xi, mi, L, reps=2)
+            rows.append(dict(config="C5", robots=n, obstacles=20, instances=inst, samples=1,
+                             members=inst, L=L, seconds=t, instances_per_s=inst / t,
+                             member_iters_per_s=inst * (L + 1) / t, smem_bytes=smem))
+            print(json.dumps(rows[-1]), flush=True)
+    with open(os.path.join(ROOT, "profiles", "r01_sweep.json"), "w") as fh:
+        json.dump({"gpu": torch.cuda.get_device_name(0), "rows": rows,
+                   "note": "device-timed solve (CUDA events), inputs resident; C5 uses 20 obstacles, "
+                           "box half-width max(1, 2 sqrt(n/32)), 1 sample, naive-prior warm start"},
+                  fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
