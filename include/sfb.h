@@ -124,6 +124,23 @@ int sfb_kinematic_peaks(const double* coeffs, int32_t n_members, int32_t n_d, in
                         int32_t n_basis, const double* Wd, const double* Wdd, int32_t k_dense,
                         double* vmax, double* amax, void* stream);
 
+/* Post-solve trajectory metrics of the reference (replaces metrics.py:48-87, compute_metrics),
+ * per member: out[b][5] = smoothness, arc_length, min_pairwise_clearance,
+ * avg_pairwise_distance, min_obstacle_clearance (inf where the reference reports inf).
+ * coeffs [B][n_d][n][n_basis]; Wdd [k_grid][n_basis] on the basis grid; W_dense
+ * [k_dense][n_basis] and t_dense [k_dense] on the dense grid (dense_basis, metrics.py:40-44);
+ * obs [n_obs][3][n_d] = center, velocity, radii[:n_d] per obstacle, member b reading
+ * obs + b * obs_member_stride (0 = shared by all members); work holds
+ * sfb_trajectory_metrics_work(...) doubles. All pointers on the device; bitwise reproducible. */
+int sfb_trajectory_metrics(const double* coeffs, int32_t n_members, int32_t n_d, int32_t n,
+                           int32_t n_basis, const double* Wdd, int32_t k_grid,
+                           const double* W_dense, const double* t_dense, int32_t k_dense,
+                           const double* obs, int32_t n_obs, int64_t obs_member_stride,
+                           double* work, double* out, void* stream);
+/* Scratch size (doubles) of sfb_trajectory_metrics, -1 if the shape is unsupported. */
+int64_t sfb_trajectory_metrics_work(int32_t n_members, int32_t n_d, int32_t n, int32_t n_basis,
+                                    int32_t k_dense);
+
 /* Dynamic shared memory one member needs (0 if the shape is unsupported). */
 int64_t sfb_smem_bytes(const sfb_plan* plan);
 

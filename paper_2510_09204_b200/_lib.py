@@ -16,7 +16,8 @@ SFB_OK, SFB_EINVAL, SFB_ESETUP, SFB_ECUDA, SFB_ENOMEM = 0, 1, 2, 3, 4
 MODE = {"projection": 0, "smoothness": 1}
 STATUS = {0: "max_iters", 1: "converged_primal", 2: "converged_fp"}
 EXPORTS = ("sfb_plan_create", "sfb_plan_destroy", "sfb_plan_cond", "sfb_solve",
-           "sfb_smem_bytes", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks")
+           "sfb_smem_bytes", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks",
+           "sfb_trajectory_metrics", "sfb_trajectory_metrics_work")
 
 
 class Dims(ctypes.Structure):
@@ -83,6 +84,12 @@ def lib() -> ctypes.CDLL:
     L.sfb_kinematic_peaks.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, vp, vp, ctypes.c_int32, vp, vp, vp]
     L.sfb_kinematic_peaks.restype = ctypes.c_int
+    i32, i64 = ctypes.c_int32, ctypes.c_int64
+    L.sfb_trajectory_metrics.argtypes = [vp, i32, i32, i32, i32, vp, i32, vp, vp, i32, vp, i32, i64,
+                                         vp, vp, vp]
+    L.sfb_trajectory_metrics.restype = ctypes.c_int
+    L.sfb_trajectory_metrics_work.argtypes = [i32, i32, i32, i32, i32]
+    L.sfb_trajectory_metrics_work.restype = ctypes.c_int64
     L.sfb_last_error.argtypes = []
     L.sfb_last_error.restype = ctypes.c_char_p
     L.sfb_abi_version.argtypes = []

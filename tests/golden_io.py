@@ -36,7 +36,9 @@ class Golden:
 
 
 def names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+    """Solver fixtures (metrics_*.npz hold the metrics epilogue's, see test_oracle.py)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if not os.path.basename(p).startswith("metrics_"))
 
 
 def load(name: str) -> Golden:

@@ -78,3 +78,39 @@ def test_kkt_blocks_match_dense_inverse():
         assert np.abs(Minv[:nv, nv:] - Mxb).max() < 1e-12 * scale
         M = np.linalg.inv(Minv)
         assert abs(np.linalg.cond(M) / sf.cond - 1) < 1e-6
+
+
+# ------------------------------------------------------------------ metrics epilogue (§8 f4)
+def _metrics_cases():
+    import glob
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(here, "metrics_*.npz")))
+
+
+def load_metrics_golden(name):
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name + ".npz"))
+    nd = int(z["n_d"])
+    obs = [(o[0, :nd], o[1, :nd], o[2, :nd]) for o in z["obstacles"]]
+    return z, nd, obs
+
+
+def metrics_close(got, ref, rtol=1e-12):
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    err = np.abs(got[fin] - ref[fin])
+    assert (err <= rtol * np.maximum(1.0, np.abs(ref[fin]))).all(), (got, ref)
+
+
+@pytest.mark.parametrize("name", _metrics_cases())
+def test_metrics_oracle_matches_reference(name):
+    """oracle/metrics.py against compute_metrics outputs of the reference (metrics.py:48-87)."""
+    from oracle.metrics import trajectory_metrics
+    z, nd, obs = load_metrics_golden(name)
+    assert len(_metrics_cases()) >= 5
+    for c, m in zip(z["coeffs"], z["metrics"]):
+        got = trajectory_metrics(c, int(z["n_basis"]), int(z["num_steps"]), float(z["duration"]),
+                                 obs, int(z["dense_factor"]))
+        metrics_close(got, m)
