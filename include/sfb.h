@@ -139,7 +139,7 @@ int sfb_trajectory_metrics(const double* coeffs, int32_t n_members, int32_t n_d,
                            double* work, double* out, void* stream);
 /* Scratch size (doubles) of sfb_trajectory_metrics, -1 if the shape is unsupported. */
 int64_t sfb_trajectory_metrics_work(int32_t n_members, int32_t n_d, int32_t n, int32_t n_basis,
-                                    int32_t k_dense);
+                                    int32_t k_dense, int32_t n_obs);
 
 /* Dynamic shared memory one member needs (0 if the shape is unsupported). */
 int64_t sfb_smem_bytes(const sfb_plan* plan);

@@ -88,7 +88,7 @@ def lib() -> ctypes.CDLL:
     L.sfb_trajectory_metrics.argtypes = [vp, i32, i32, i32, i32, vp, i32, vp, vp, i32, vp, i32, i64,
                                          vp, vp, vp]
     L.sfb_trajectory_metrics.restype = ctypes.c_int
-    L.sfb_trajectory_metrics_work.argtypes = [i32, i32, i32, i32, i32]
+    L.sfb_trajectory_metrics_work.argtypes = [i32, i32, i32, i32, i32, i32]
     L.sfb_trajectory_metrics_work.restype = ctypes.c_int64
     L.sfb_last_error.argtypes = []
     L.sfb_last_error.restype = ctypes.c_char_p

@@ -87,7 +87,7 @@ def metrics_batch(coeffs_mm, basis, obstacles=None, dense_factor: int = 10, devi
     obs, stride = _obstacle_array(obstacles, n_d, B)
     n_obs = obs.shape[-3] if obs.size else 0
     L = _lib.lib()
-    nwork = L.sfb_trajectory_metrics_work(B, n_d, n, nb, dense.W.shape[0])
+    nwork = L.sfb_trajectory_metrics_work(B, n_d, n, nb, dense.W.shape[0], n_obs)
     if nwork < 0:
         raise ShapeError("problem shape unsupported by sfb_trajectory_metrics")
     host = [np.ascontiguousarray(a, float).ravel() for a in (basis.Wdd, dense.W, dense.grid, obs)]
