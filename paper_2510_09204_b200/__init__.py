@@ -14,5 +14,7 @@ from .solver import (BatchResult, DeviceBatch, KktCache, ObjectiveMode, SolverCo
                      fixed_point_step, kinematic_peaks, primal_residual, rank_candidates,
                      solve, solve_batch, solve_instances, state_from_xi, time_scale_batch,
                      time_scale_for_limits)
+from .metrics import TrajectoryMetrics, compute_metrics, dense_basis, metrics_batch
+from .pipeline import CandidateBatch, PlanResult, plan, plan_many
 
 __version__ = "0.1.0"

@@ -36,9 +36,9 @@ class Golden:
 
 
 def names():
-    """Solver fixtures (metrics_*.npz hold the metrics epilogue's, see test_oracle.py)."""
+    """Solver fixtures (metrics_*.npz / plan_*.npz belong to the epilogue and planner tests)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if not os.path.basename(p).startswith("metrics_"))
+                  if not os.path.basename(p).startswith(("metrics_", "plan_")))
 
 
 def load(name: str) -> Golden:
