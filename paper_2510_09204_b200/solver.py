@@ -175,8 +175,31 @@ def _kron_checked(A: np.ndarray, n: int, E: np.ndarray) -> bool:
     return ok
 
 
+_SD: dict = {}
+
+
 def system_data(sys, kind: str = "projection", rho: float = 1.0) -> SystemData:
-    """Extract and validate the structured data of a (reference or local) ConstraintSystem."""
+    """Extract and validate the structured data of a (reference or local) ConstraintSystem.
+
+    Memoised per system object (weak reference + identities of its arrays): like the reference's
+    KktCache (solver.py:64-91), a ConstraintSystem is treated as immutable once built."""
+    import weakref
+    arrs = (sys.A, sys.b, sys.h, sys.obs_pos, sys.obs_axes, sys.pair_axes, sys.basis.W)
+    ident = tuple(map(id, arrs))
+    hit = _SD.get(id(sys))
+    if hit is not None and hit[0]() is sys and hit[1] == ident and hit[2] == float(sys.d_max):
+        return hit[3]
+    sd = _system_data(sys, kind, rho)
+    if len(_SD) > 4096:
+        _SD.clear()
+    try:
+        _SD[id(sys)] = (weakref.ref(sys), ident, float(sys.d_max), sd)
+    except TypeError:                     # object without weakref support: no memo
+        pass
+    return sd
+
+
+def _system_data(sys, kind: str, rho: float) -> SystemData:
     d = sys.dims
     n, n_d, n_xi, K1, m = d.n, d.n_d, d.n_basis, d.num_steps, d.n_obs
     A = np.asarray(sys.A, float)
@@ -301,20 +324,21 @@ def _as_tensor(x, device, dtype, counter=None):
     return t.to(device)
 
 
-_PINNED = {"buf": None}
+_PINNED: dict = {}
 
 
-def _pinned(n: int):
-    """Grow-only pinned host staging buffer (float64) for the input arena."""
+def _pinned(n: int, which: str = "in"):
+    """Grow-only pinned host staging buffers (float64): the input arena ("in") and the
+    output copies ("out", "trace"). Each use is synchronous, so reuse is safe."""
     import torch
-    buf = _PINNED["buf"]
+    buf = _PINNED.get(which)
     if buf is None or buf.numel() < n:
         size = max(n, 1 << 16)
         try:
             buf = torch.empty(size, dtype=torch.float64).pin_memory()
         except RuntimeError:                      # no CUDA context yet / no pinning available
             buf = torch.empty(size, dtype=torch.float64)
-        _PINNED["buf"] = buf
+        _PINNED[which] = buf
     return buf
 
 
@@ -348,13 +372,25 @@ class DeviceBatch:
         f64, dev = torch.float64, self.device
         # ---- inputs: host arrays are packed into one buffer and cross PCIe in one copy;
         # CUDA tensors (e.g. straight from a PyTorch sampler) are used in place
-        host_parts, dev_parts = [], {}
+        host_parts, dev_parts, uploaded = [], {}, {}
+        direct_bytes = 0
 
         def add(name, x, shape, dtype=np.float64):
+            nonlocal direct_bytes
             if isinstance(x, torch.Tensor) and x.is_cuda:
                 t = x.to(device=dev, dtype=torch.float64 if dtype == np.float64 else torch.int32)
                 dev_parts[name] = t.contiguous()
                 return tuple(t.shape)
+            if (isinstance(x, torch.Tensor) and dtype == np.float64 and x.dtype == torch.float64
+                    and x.is_contiguous() and x.is_pinned()):
+                # pinned host tensor: one DMA straight from it (the same tensor passed as
+                # xi0 and target crosses once)
+                key = (x.data_ptr(), tuple(x.shape))
+                if key not in uploaded:
+                    uploaded[key] = x.to(dev)
+                    direct_bytes += x.numel() * 8
+                dev_parts[name] = uploaded[key]
+                return tuple(x.shape)
             a = x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x
             a = np.ascontiguousarray(np.asarray(a, dtype=dtype))
             host_parts.append((name, a))
@@ -400,7 +436,7 @@ class DeviceBatch:
             o, _ = offs[name]
             arena_h[o: o + a.size] = a.reshape(-1)
         self._in_arena = staging[:total].to(dev)       # synchronous copy from pinned memory
-        self.h2d_bytes = int(arena_h.nbytes)
+        self.h2d_bytes = int(arena_h.nbytes) + direct_bytes
         views = {}
         for name, (o, shp) in offs.items():
             views[name] = self._in_arena[o: o + int(np.prod(shp))].view(shp)
@@ -471,7 +507,9 @@ class DeviceBatch:
         only up to the longest member's iterations). Member-major arrays."""
         import torch
         B, n_d, n, n_xi = self.out_xi.shape
-        head = self._out_arena[: self._out_prefix].cpu().numpy()
+        head = _pinned(self._out_prefix, "out")[: self._out_prefix]
+        head.copy_(self._out_arena[: self._out_prefix])
+        head = head.numpy()
         o = self._oofs
         get = lambda k: head[o[k][0]: o[k][0] + o[k][1]]
         its = get("its").view(np.int32)[:B].copy()
@@ -484,7 +522,9 @@ class DeviceBatch:
         d2h = head.nbytes
         if self.out_trace is not None:
             T = int(its.max()) + 1 if its.size else 0
-            tr = self.out_trace[:, :T].cpu().numpy()
+            tr = _pinned(B * T * 2, "trace")[: B * T * 2].view(B, T, 2)
+            tr.copy_(self.out_trace[:, :T])
+            tr = tr.numpy().copy()
             d2h += tr.nbytes
             out["trace"] = [tr[b, : its[b] + 1] for b in range(B)]
         if self.out_counters is not None:
