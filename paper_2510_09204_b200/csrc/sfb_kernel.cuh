@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sfb {
 
 #ifndef SFB_MAXW
@@ -625,33 +627,39 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
 #endif
         if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
-        while (mask) {
-          const int o = o0 + __ffs(mask) - 1;
-          mask &= mask - 1u;
-          const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
+        // exact rows of the flagged obstacles; static and moving obstacles in separate loops so
+        // the static path issues no (speculative) global load of the track
+        auto obs_rows = [&](auto is_static) {
+          constexpr bool ST = decltype(is_static)::value;
+          while (mask) {
+            const int o = o0 + __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            if (kk < nsteps) {
-              const int k = 2 * kg + kk;
-              double d[ND], r[ND];
+            for (int kk = 0; kk < 2; ++kk) {
+              if (kk < nsteps) {
+                const int k = 2 * kg + kk;
+                double d[ND], r[ND];
 #pragma unroll
-              for (int a = 0; a < ND; ++a)
-                d[a] = p[a][kk] - (P.obs_static ? sObsC[o * ND + a]
-                                                : __ldg(opos + ((size_t)a * m + o) * K1 + k));
-              ++c_exact;
-              if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
-                ++c_active;
-                double rr = 0.0;
+                for (int a = 0; a < ND; ++a)
+                  d[a] = p[a][kk] - (ST ? sObsC[o * ND + a] : __ldg(opos + ((size_t)a * m + o) * K1 + k));
+                ++c_exact;
+                if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
+                  ++c_active;
+                  double rr = 0.0;
 #pragma unroll
-                for (int a = 0; a < ND; ++a) {
-                  g[a][kk] += r[a];
-                  rr = fma(r[a], r[a], rr);
+                  for (int a = 0; a < ND; ++a) {
+                    g[a][kk] += r[a];
+                    rr = fma(r[a], r[a], rr);
+                  }
+                  s1 += rr;
                 }
-                s1 += rr;
               }
             }
           }
-        }
+        };
+        if (P.obs_static) obs_rows(std::true_type{});
+        else obs_rows(std::false_type{});
       }
 
       SFB_TSUB(9);
