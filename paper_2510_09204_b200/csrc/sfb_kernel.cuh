@@ -138,6 +138,36 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
   return true;
 }
 
+// ---- DSMEM exchange primitives (sm_90+): stores into a peer CTA's shared memory that
+// complete a transaction count on the peer's mbarrier, so the receiver waits for its data
+// instead of the whole cluster meeting at a barrier (which also costs a GPU-scope fence)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t addr, double a, double b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(addr), "d"(a), "d"(b), "r"(bar) : "memory");
+}
+// cluster exchange geometry: the G vector plus (S1, S2), padded to even length, in csize
+// slices of SL (even) doubles; slice r has slice_len(r) live entries
+__host__ __device__ inline int xch_tot(int nv) { return (nv + 3) & ~1; }
+__host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) + csize - 1) / csize + 1) & ~1; }
+
 #ifndef SFB_MINB
 #define SFB_MINB 2
 #endif
@@ -329,6 +359,18 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   if (obs_axmin < INFINITY) atomicMin(&sMisc[1], __float_as_uint(obs_axmin));
   __syncthreads();
   obs_absmax = __uint_as_float(sMisc[0]);
+  // cluster exchange: receive buffer [csize][SL] then two mbarriers (reduce-scatter, all-gather)
+  const int xtot = xch_tot(nv), xSL = xch_sl(nv, csize);
+  double* xrecv = reinterpret_cast<double*>(smem + P.L.xg);
+  const uint32_t xbar1 = smem_u32(xrecv + (size_t)csize * xSL), xbar2 = xbar1 + 8;
+  if (csize > 1) {
+    if (tid == 0) {
+      mbar_init(xbar1, 1);
+      mbar_init(xbar2, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cooperative_groups::this_cluster().sync();   // peers started and their barriers exist
+  }
 
   double box_lo[ND], box_hi[ND];
 #pragma unroll
@@ -772,42 +814,44 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       FP += sRed[w * 4 + 3];
     }
     if (csize > 1) {
-      // Cluster reduction of the CTA partials (G and S1, S2) in two pushes over DSMEM:
-      //  1. reduce-scatter: the partial slice s goes to rank s's receive buffer,
+      // Cluster reduction of the CTA partials (G and S1, S2) in two DSMEM pushes, each
+      // completing on the receiver's mbarrier (st.async ... complete_tx):
+      //  1. reduce-scatter: slice s of the partial goes to rank s's receive buffer,
       //  2. rank s sums its slice over the ranks in rank order and stores the sum into every
       //     rank's G (whose local partial was already scattered in step 1).
-      // A cluster barrier follows each push; the receive buffer of step t is read before
-      // barrier 2 of step t, so no buffer is rewritten while it can still be read.
-      auto cluster = cooperative_groups::this_cluster();
-      const int tot = nv + 2, SL = (tot + csize - 1) / csize;
-      double* recv = reinterpret_cast<double*>(smem + P.L.xg);   // [csize][SL]
+      // No cluster barrier is needed to reuse a buffer: a rank's next push into it depends on
+      // data the buffer's owner sends only after it has consumed the buffer.
+      const uint32_t par = (uint32_t)(it & 1);
+      auto slice_len = [&](int r) { return max(0, min(xSL, xtot - r * xSL)); };
       if (tid == 0) {
         sG[nv] = S1;
         sG[nv + 1] = S2;
+        if (xtot > nv + 2) sG[nv + 2] = 0.0;
+        mbar_expect_tx(xbar1, (uint32_t)(csize * slice_len(crank) * 8));
       }
       __syncthreads();
 #ifdef SFB_PHASE_TIMING
       if (tid == 0) t_sub = clock64();
 #endif
-      for (int o = tid; o < tot; o += nt) {
-        const int sr = o / SL;
-        cluster.map_shared_rank(recv, sr)[crank * SL + (o - sr * SL)] = sG[o];
+      for (int o = 2 * tid; o < xtot; o += 2 * nt) {
+        const int sr = o / xSL;
+        st_async_v2(dsmem_map(smem_u32(xrecv + (size_t)crank * xSL + (o - sr * xSL)), sr), sG[o], sG[o + 1],
+                    dsmem_map(xbar1, sr));
       }
-      cluster.sync();
+      mbar_wait(xbar1, par);
       SFB_TSUB(11);
-      double* gr[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) gr[r] = cluster.map_shared_rank(sG, r < csize ? r : 0);
-      for (int j = tid; j < SL; j += nt) {
-        const int o = crank * SL + j;
-        if (o >= tot) break;
-        double acc = 0.0;
-        for (int r = 0; r < csize; ++r) acc += recv[r * SL + j];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (r < csize) gr[r][o] = acc;
+      if (tid == 0) mbar_expect_tx(xbar2, (uint32_t)(xtot * 8));
+      const int mylen = slice_len(crank);
+      for (int j = 2 * tid; j < mylen; j += 2 * nt) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int r = 0; r < csize; ++r) {
+          a0 += xrecv[(size_t)r * xSL + j];
+          a1 += xrecv[(size_t)r * xSL + j + 1];
+        }
+        const uint32_t dst = smem_u32(sG + crank * xSL + j);
+        for (int r = 0; r < csize; ++r) st_async_v2(dsmem_map(dst, r), a0, a1, dsmem_map(xbar2, r));
       }
-      cluster.sync();
+      mbar_wait(xbar2, par);
       SFB_TSUB(12);
       S1 = sG[nv];
       S2 = sG[nv + 1];
