@@ -36,6 +36,7 @@ namespace sfb {
 #define SFB_MAXW 8
 #endif
 constexpr int NW = SFB_MAXW;     // max warps per CTA (the launch uses P.nw <= NW)
+constexpr int NBM = 6;           // max boundary rows per robot (rest-to-rest; 2 otherwise)
 constexpr int NT = NW * 32;      // max threads per CTA
 constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1 or dummy body) position in shared memory
 constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -> never a hit
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   const int crank = csize > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
   const int b = blockIdx.x / csize;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = P.nw, nt = nw * 32;
+  const int nw = BIG ? P.nw : NW, nt = nw * 32;   // n <= 32 always runs NW warps (compile-time strides)
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
   const int nv = ND * n * NXI;       // dense outputs per member
   const int nrows = ND * n;          // (axis, robot) rows
@@ -808,7 +809,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     SFB_TMARK(2);
     // -------------------------------------------- D: residuals, trace, convergence
     double S1 = 0.0, S2 = 0.0, FP = 0.0;
-    for (int w = 0; w < nw; ++w) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      if (w >= nw) break;
       S1 += sRed[w * 4 + 0];
       S2 += sRed[w * 4 + 1];
       FP += sRed[w * 4 + 3];
@@ -884,7 +887,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         for (int off = 16; off > 0; off >>= 1) eqp = fmax(eqp, __shfl_xor_sync(FULL, eqp, off));
         if (lane == 0) sRed[warp * 4 + 2] = eqp;
         __syncthreads();
-        for (int w = 0; w < nw; ++w) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
+        #pragma unroll
+        for (int w = 0; w < NW; ++w)
+          if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
       }
       double* xo = P.xi + (size_t)b * nv;
       double* lo = P.lam + (size_t)b * nv;
@@ -913,7 +918,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       double csum = 0.0;
       if (col < ncolD) {
         const int a = col / NXI, c = col - a * NXI;
-        for (int i0 = 0; i0 < n; i0 += 32) {
+        for (int i0 = 0; i0 < (BIG ? n : 1); i0 += 32) {   // n <= 32: one pass
           const int ii = i0 + lane;
           if (ii < n) {
             const int ai = a * n + ii;
@@ -939,7 +944,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
       } else {
         const int t2 = col - ncolD, a = t2 / NB, r = t2 - a * NB;
-        for (int i0 = 0; i0 < n; i0 += 32) {
+        for (int i0 = 0; i0 < (BIG ? n : 1); i0 += 32) {   // n <= 32: one pass
           const int ii = i0 + lane;
           if (ii < n) {
             const int ai = a * n + ii;
@@ -967,7 +972,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     __syncthreads();
     SFB_TMARK(4);
     if (it > 0) {
-      for (int w = 0; w < nw; ++w) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
+      #pragma unroll
+        for (int w = 0; w < NW; ++w)
+          if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
     }
     // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp
     for (int col = warp; col < ncolD; col += nw) {
@@ -975,9 +982,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       double m0 = 0.0, m1 = 0.0;
 #pragma unroll
       for (int c2 = 0; c2 < NXI; ++c2) m0 = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], m0);
-      for (int r = 0; r < NB; ++r) m1 = fma(sDxb[c * NB + r], sSU[a * NB + r], m1);
+#pragma unroll
+      for (int r = 0; r < NBM; ++r)
+        if (r < NB) m1 = fma(sDxb[c * NB + r], sSU[a * NB + r], m1);
       const double mean = m0 + m1;
-      for (int i0 = 0; i0 < n; i0 += 32) {
+      for (int i0 = 0; i0 < (BIG ? n : 1); i0 += 32) {   // n <= 32: one pass
         const int ii = i0 + lane;
         if (ii < n) {
           const int ai = a * n + ii;
@@ -990,7 +999,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
             acc1 = fma(sPxx[c * NXI + c2 + 1], dv[c2 + 1], acc1);
           }
           if (NXI & 1) acc0 = fma(sPxx[c * NXI + NXI - 1], dv[NXI - 1], acc0);
-          for (int r = 0; r < NB; ++r) acc1 = fma(sPxb[c * NB + r], uv[r], acc1);
+#pragma unroll
+          for (int r = 0; r < NBM; ++r)
+            if (r < NB) acc1 = fma(sPxb[c * NB + r], uv[r], acc1);
           const double xo = sXi[ai * NXP + c];
           const double xn = xo + ((acc0 + acc1) + mean);
           sXi[ai * NXP + c] = xn;
