@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           }
         }
       } else {
-        const int t2 = col - ncolD, a = t2 / NB, r = t2 - a * NB;
+        const int t2 = col - ncolD, a = (t2 >= NB) + (ND == 3 && t2 >= 2 * NB), r = t2 - a * NB;
         for (int i0 = 0; i0 < (BIG ? n : 1); i0 += 32) {   // n <= 32: one pass
           const int ii = i0 + lane;
           if (ii < n) {
