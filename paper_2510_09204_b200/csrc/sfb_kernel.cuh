@@ -41,9 +41,11 @@ constexpr int NT = NW * 32;      // max threads per CTA
 constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1 or dummy body) position in shared memory
 constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -> never a hit
 constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the reference evaluates it
+constexpr int GRID = 32;         // obstacle candidate grid cells per axis (compact mode)
 
 struct Layout {       // byte offsets into dynamic shared memory
   int xi, lam, tgt, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs_s, obs, pmax, gl, uni;
+  int grid;           // static-obstacle candidate grid [GRID][GRID] u32 (compact mode)
   int xg;             // cluster exchange buffers [2][nv + 2] (set at launch when csize > 1)
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
@@ -51,6 +53,7 @@ struct Layout {       // byte offsets into dynamic shared memory
 
 struct KParams {
   int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
+  int compact;     // n <= 32, MP <= 32: compacted exact rows + obstacle grid (static obstacles)
   int kgs;         // n > 32: k-group rows of positions held per CTA (its time slice)
   int csize;       // CTAs per member (thread-block cluster along the time axis), 1..8
   int mode, max_iters, early_exit;
@@ -104,7 +107,7 @@ __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fa
 // append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
 __device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __funnelshift_l(t, m, 1); }
 
-// 1/sqrt(q) in FP64 from the FP32 MUFU seed and one Newton step (relative error ~1e-14,
+// 1/sqrt(q) in FP64 from the FP32 MUFU seed and one Newton step (relative error ~1e-14,  // @stage exact_math
 // vs ~1e-16 for rsqrt(double); the seed needs q inside the FP32 normal range)
 __device__ __forceinline__ double rsqrt_fast(double q) {
   if (!(q > 1e-30 && q < 1e30)) return rsqrt(q);
@@ -139,7 +142,7 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
   return true;
 }
 
-// ---- DSMEM exchange primitives (sm_90+): stores into a peer CTA's shared memory that
+// ---- DSMEM exchange primitives (sm_90+): stores into a peer CTA's shared memory that  // @stage cluster_prims
 // complete a transaction count on the peer's mbarrier, so the receiver waits for its data
 // instead of the whole cluster meeting at a barrier (which also costs a GPU-scope fence)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -203,7 +206,7 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
 template <int ND, int NXI, int NJ, bool BIG>
-__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {
+__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
@@ -360,6 +363,44 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   if (obs_axmin < INFINITY) atomicMin(&sMisc[1], __float_as_uint(obs_axmin));
   __syncthreads();
   obs_absmax = __uint_as_float(sMisc[0]);
+  // compact mode (n <= 32, static obstacles): flagged rows are computed lane-parallel from a
+  // per-task entry list, and obstacle rows are nominated by a grid over the obstacles' (x, y)
+  // contact discs instead of an FP32 test of every obstacle. A cell lists obstacle o if its
+  // rectangle, widened by 1e-3 of a cell, meets the disc of radius 1.001 a_o + 1e-6 around
+  // the centre: every row the FP32 screen could flag (|p - c| < a sqrt(1 + 2e-3) with FP32
+  // positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a, so no active row is lost.
+  const bool compact = !BIG && P.compact && (m == 0 || P.obs_static);
+  unsigned* sGrid = reinterpret_cast<unsigned*>(smem + P.L.grid);
+  float gx0 = 0.f, gy0 = 0.f, gix = 0.f, giy = 0.f;
+  if (compact && m > 0) {
+    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (int o = 0; o < m; ++o) {
+      const double rg = sObsAx[o * 4 + 2] * 1.001 + 1e-6;
+      x0 = fmin(x0, sObsC[o * ND] - rg);
+      x1 = fmax(x1, sObsC[o * ND] + rg);
+      y0 = fmin(y0, sObsC[o * ND + 1] - rg);
+      y1 = fmax(y1, sObsC[o * ND + 1] + rg);
+    }
+    const double hx = (x1 - x0) / GRID, hy = (y1 - y0) / GRID;
+    gx0 = (float)x0;
+    gy0 = (float)y0;
+    gix = (float)(1.0 / hx);
+    giy = (float)(1.0 / hy);
+    for (int cidx = tid; cidx < GRID * GRID; cidx += nt) {
+      const int cy = cidx / GRID, cx = cidx - cy * GRID;
+      const double rx0 = x0 + cx * hx - 1e-3 * hx, rx1 = x0 + (cx + 1) * hx + 1e-3 * hx;
+      const double ry0 = y0 + cy * hy - 1e-3 * hy, ry1 = y0 + (cy + 1) * hy + 1e-3 * hy;
+      unsigned bits = 0u;
+      for (int o = 0; o < m; ++o) {
+        const double ox = sObsC[o * ND], oy = sObsC[o * ND + 1];
+        const double dx = fmin(fmax(ox, rx0), rx1) - ox, dy = fmin(fmax(oy, ry0), ry1) - oy;
+        const double rg = sObsAx[o * 4 + 2] * 1.001 + 1e-6;
+        if (dx * dx + dy * dy <= rg * rg) bits |= 1u << o;
+      }
+      sGrid[cidx] = bits;
+    }
+    __syncthreads();
+  }
   // cluster exchange: receive buffer [csize][SL] then two mbarriers (reduce-scatter, all-gather)
   const int xtot = xch_tot(nv), xSL = xch_sl(nv, csize);
   double* xrecv = reinterpret_cast<double*>(smem + P.L.xg);
@@ -378,6 +419,13 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   for (int a = 0; a < ND; ++a) {
     box_lo[a] = P.box[((size_t)inst * 2 + 0) * ND + a];
     box_hi[a] = P.box[((size_t)inst * 2 + 1) * ND + a];
+  }
+  float blo_f[ND], bhi_f[ND];
+#pragma unroll
+  for (int a = 0; a < ND; ++a) {
+    const float bmg = 1e-4f * (1.f + (float)fmax(fabs(box_lo[a]), fabs(box_hi[a])));
+    blo_f[a] = (float)box_lo[a] + bmg;
+    bhi_f[a] = (float)box_hi[a] - bmg;
   }
   const double ra = P.pair_axes[(size_t)inst * 3 + 0], rb_ax = P.pair_axes[(size_t)inst * 3 + 2];
   const double r_inv_a2 = 1.0 / (ra * ra), r_inv_b2 = 1.0 / (rb_ax * rb_ax);
@@ -415,7 +463,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   double eq_max = 0.0;
   unsigned long long c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
-  for (int it = 0;; ++it) {
+  for (int it = 0;; ++it) {  // @stage iter_top
     // -------------------------------------------- A/B/C per k-group task
     constexpr bool GREG = BIG || SFB_GREG;   // partials held in registers
     double Gp[GREG ? ND : 1][GREG ? NXI : 1];
@@ -443,7 +491,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       if (tid == 0) t_sub = clock64();
 #endif
 
-      // A: exact positions of the lane's robot at the two steps
+      // A: exact positions of the lane's robot at the two steps  // @stage A_positions
       double p[ND][2];
 #pragma unroll
       for (int a = 0; a < ND; ++a) p[a][0] = p[a][1] = 0.0;
@@ -516,200 +564,249 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       const int nsteps = live ? (has1 ? 2 : 1) : 0;
       SFB_TSUB(6);
 
-      double g[ND][2];
+      double g[ND][2];  // @stage B_pair_screen
 #pragma unroll
       for (int a = 0; a < ND; ++a) g[a][0] = g[a][1] = 0.0;
 
-      // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
-      for (int j0 = 0; j0 < (BIG ? n : 1); j0 += 32) {
-        const int jc = BIG ? min(32, n - j0) : n;
-        unsigned mask = 0u;
-        if (!force) {
-          const float2 thr2 = make_float2(-r_thr, -r_thr);
-          const float* base = BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + j0) * ND2 : posw;
-          unsigned mm = 0u;
-          auto screen = [&](const float* bp) {
-            const float4 v = *reinterpret_cast<const float4*>(bp);
-            const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-            const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-            float2 q = __ffma2_rn(dy, dy, thr2);
-            q = __ffma2_rn(dx, dx, q);
-            if (ND == 3) {
-              const float4 v2 = *reinterpret_cast<const float4*>(bp + 4);
-              const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-              q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
-            }
-            mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
-          };
-          if (BIG) {
-#pragma unroll 4
-            for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2);
-            mask = __brev(mm) >> (32 - jc);
-          } else {
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) screen(base + j * ND2);
-            mask = (__brev(mm) >> (32 - NJ)) & ((jc >= 32) ? FULL : ((1u << jc) - 1u));
+      // pair screen of one chunk of 32 bodies: bit j set if body j0 + j may be within contact
+      auto pair_screen = [&](int j0, int jc) -> unsigned {
+        const float2 thr2 = make_float2(-r_thr, -r_thr);
+        const float* base = BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + j0) * ND2 : posw;
+        unsigned mm = 0u;
+        auto screen = [&](const float* bp) {
+          const float4 v = *reinterpret_cast<const float4*>(bp);
+          const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+          const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+          float2 q = __ffma2_rn(dy, dy, thr2);
+          q = __ffma2_rn(dx, dx, q);
+          if (ND == 3) {
+            const float4 v2 = *reinterpret_cast<const float4*>(bp + 4);
+            const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+            q = __ffma2_rn(__fmul2_rn(dz, make_float2(r_kap, r_kap)), dz, q);
           }
-        } else {
-          mask = (jc >= 32) ? FULL : ((1u << jc) - 1u);
-        }
-        if (i >= j0 && i < j0 + jc) mask &= ~(1u << (i - j0));
-        if (!live) mask = 0u;
-#ifdef SFB_EXP_NOEXACT
-        if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;   // timing ablation only
-#endif
-        if (P.counters) c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
-        SFB_TSUB(7);
-
-        // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)
-        while (__any_sync(FULL, mask != 0u)) {
-          const bool act = mask != 0u;
-          const int jl = act ? __ffs(mask) - 1 : 0;
-          mask &= mask - 1u;
-          const int j = j0 + jl;
-          double pj[ND][2];
-          if (BIG) {
-            const float* hp = sPos + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
-            const float* lp = sLo + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
-#pragma unroll
-            for (int a = 0; a < ND; ++a)
-#pragma unroll
-              for (int kk = 0; kk < 2; ++kk)
-                pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
-          } else {
-            const int src = sub * LW + jl;
-#pragma unroll
-            for (int a = 0; a < ND; ++a)
-#pragma unroll
-              for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
-          }
-          if (act) {
-            const double cs = (i < j) ? 1.0 : -1.0;
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              if (kk < nsteps) {
-                double d[ND], r[ND];
-#pragma unroll
-                for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
-                ++c_exact;
-                if (row_exact<ND>(d, r_inv_a2, r_inv_b2, ra, rb_ax, d_max, cs, r)) {
-                  if (i < j) ++c_active;   // each pair row once, like the reference's F rows
-                  double rr = 0.0;
-#pragma unroll
-                  for (int a = 0; a < ND; ++a) {
-                    g[a][kk] += r[a];
-                    rr = fma(r[a], r[a], rr);
-                  }
-                  if (i < j) s1 += rr;
-                }
-              }
-            }
-          }
-        }
-      }
-
-      SFB_TSUB(8);
-      // B: obstacles (padded to MP), in chunks of 32
-#ifdef SFB_EXP_NOOBS
-      for (int o0 = 0; o0 < 0; o0 += 32) {
-#else
-      for (int o0 = 0; o0 < MP; o0 += 32) {
-#endif
-        const int oc = min(32, MP - o0);
-        unsigned mask = 0u;
-        if (!force) {
-          unsigned mm = 0u;
-          if (P.obs_static) {
-            // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
-            const float* ob = sObsS + (size_t)o0 * OS;
-            for (int o4 = 0; o4 < oc; o4 += 4)   // MP is a multiple of 4
-#pragma unroll
-            for (int o = o4; o < o4 + 4; ++o) {
-              const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
-              const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
-              const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
-              float2 q;
-              if (ND == 3) {
-                const float4 v2 = *reinterpret_cast<const float4*>(ob + o * OS + 4);
-                const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
-                                             make_float2(own[ND - 1][0], own[ND - 1][1]));
-                q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
-                q = __ffma2_rn(dy, dy, q);
-              } else {
-                q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
-              }
-              q = __ffma2_rn(dx, dx, q);
-              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
-            }
-          } else {
-            const float* obase = sObs + ((size_t)kg * MP + o0) * ND2;
-#pragma unroll 4
-            for (int o = 0; o < oc; ++o) {
-              const float4 v = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2);
-              const float th = sObsThr[o0 + o];
-              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-              float2 q = __ffma2_rn(dy, dy, make_float2(-th, -th));
-              q = __ffma2_rn(dx, dx, q);
-              if (ND == 3) {
-                const float kp = sObsThr[MP + o0 + o];
-                const float4 v2 = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2 + 4);
-                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-                q = __ffma2_rn(__fmul2_rn(dz, make_float2(kp, kp)), dz, q);
-              }
-              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
-            }
-          }
-          mask = __brev(mm) >> (32 - oc);
-        } else {
-          const int ov = max(0, min(32, m - o0));
-          mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
-        }
-        if (!live) mask = 0u;
-#ifdef SFB_EXP_NOEXACT
-        if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
-#endif
-        if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
-        // exact rows of the flagged obstacles; static and moving obstacles in separate loops so
-        // the static path issues no (speculative) global load of the track
-        auto obs_rows = [&](auto is_static) {
-          constexpr bool ST = decltype(is_static)::value;
-          while (mask) {
-            const int o = o0 + __ffs(mask) - 1;
-            mask &= mask - 1u;
-            const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              if (kk < nsteps) {
-                const int k = 2 * kg + kk;
-                double d[ND], r[ND];
-#pragma unroll
-                for (int a = 0; a < ND; ++a)
-                  d[a] = p[a][kk] - (ST ? sObsC[o * ND + a] : __ldg(opos + ((size_t)a * m + o) * K1 + k));
-                ++c_exact;
-                if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
-                  ++c_active;
-                  double rr = 0.0;
-#pragma unroll
-                  for (int a = 0; a < ND; ++a) {
-                    g[a][kk] += r[a];
-                    rr = fma(r[a], r[a], rr);
-                  }
-                  s1 += rr;
-                }
-              }
-            }
-          }
+          mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
         };
-        if (P.obs_static) obs_rows(std::true_type{});
-        else obs_rows(std::false_type{});
+        if constexpr (BIG) {
+#pragma unroll 4
+          for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2);
+          return __brev(mm) >> (32 - jc);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) screen(base + j * ND2);
+          return (__brev(mm) >> (32 - NJ)) & ((jc >= 32) ? FULL : ((1u << jc) - 1u));
+        }
+      };
+
+      {
+        // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
+        for (int j0 = 0; j0 < (BIG ? n : 1); j0 += 32) {
+          const int jc = BIG ? min(32, n - j0) : n;
+          unsigned mask = 0u;
+          if (!force) {
+            mask = pair_screen(j0, jc);
+          } else {
+            mask = (jc >= 32) ? FULL : ((1u << jc) - 1u);
+          }
+          if (i >= j0 && i < j0 + jc) mask &= ~(1u << (i - j0));
+          if (!live) mask = 0u;
+#ifdef SFB_EXP_NOEXACT
+          if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;   // timing ablation only
+#endif
+          if (P.counters) c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
+          SFB_TSUB(7);
+
+          // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)  // @stage B_pair_exact
+          while (__any_sync(FULL, mask != 0u)) {
+            const bool act = mask != 0u;
+            const int jl = act ? __ffs(mask) - 1 : 0;
+            mask &= mask - 1u;
+            const int j = j0 + jl;
+            double pj[ND][2];
+            if (BIG) {
+              const float* hp = sPos + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
+              const float* lp = sLo + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
+#pragma unroll
+              for (int a = 0; a < ND; ++a)
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk)
+                  pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
+            } else {
+              const int src = sub * LW + jl;
+#pragma unroll
+              for (int a = 0; a < ND; ++a)
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+            }
+            if (act) {
+              const double cs = (i < j) ? 1.0 : -1.0;
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                if (kk < nsteps) {
+                  double d[ND], r[ND];
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
+                  ++c_exact;
+                  if (row_exact<ND>(d, r_inv_a2, r_inv_b2, ra, rb_ax, d_max, cs, r)) {
+                    if (i < j) ++c_active;   // each pair row once, like the reference's F rows
+                    double rr = 0.0;
+#pragma unroll
+                    for (int a = 0; a < ND; ++a) {
+                      g[a][kk] += r[a];
+                      rr = fma(r[a], r[a], rr);
+                    }
+                    if (i < j) s1 += rr;
+                  }
+                }
+              }
+            }
+          }
+        }
+
+        SFB_TSUB(8);  // @stage B_obs_screen
+        // B: obstacles (padded to MP), in chunks of 32
+#ifdef SFB_EXP_NOOBS
+        for (int o0 = 0; o0 < 0; o0 += 32) {
+#else
+        for (int o0 = 0; o0 < MP; o0 += 32) {
+#endif
+          const int oc = min(32, MP - o0);
+          unsigned mask = 0u;
+          if (!force) {
+            unsigned mm = 0u;
+            if (compact) {
+              // grid candidates of the lane's two positions, each confirmed by the FP32 test
+              // (per lane: a robot is near few obstacles)
+              auto cell = [&](float x, float y) -> unsigned {
+                const int cx = __float2int_rd((x - gx0) * gix), cy = __float2int_rd((y - gy0) * giy);
+                return ((unsigned)cx < (unsigned)GRID && (unsigned)cy < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
+              };
+              unsigned cand = live ? cell(own[0][0], own[1][0]) : 0u;
+              if (live && has1) cand |= cell(own[0][1], own[1][1]);
+              while (cand) {
+                const int o = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                const float4 v = *reinterpret_cast<const float4*>(sObsS + o * OS);
+                const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
+                const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
+                float2 q;
+                if (ND == 3) {
+                  const float4 v2 = *reinterpret_cast<const float4*>(sObsS + o * OS + 4);
+                  const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
+                                               make_float2(own[ND - 1][0], own[ND - 1][1]));
+                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
+                  q = __ffma2_rn(dy, dy, q);
+                } else {
+                  q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
+                }
+                q = __ffma2_rn(dx, dx, q);
+                if ((int)(__float_as_uint(q.x) | __float_as_uint(q.y)) < 0) mm |= 1u << o;
+              }
+              mm = __brev(mm << (32 - oc));   // undone by the shared bit reversal below
+            } else if (P.obs_static) {
+              // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
+              const float* ob = sObsS + (size_t)o0 * OS;
+              for (int o4 = 0; o4 < oc; o4 += 4)   // MP is a multiple of 4
+#pragma unroll
+              for (int o = o4; o < o4 + 4; ++o) {
+                const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
+                const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
+                const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
+                float2 q;
+                if (ND == 3) {
+                  const float4 v2 = *reinterpret_cast<const float4*>(ob + o * OS + 4);
+                  const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
+                                               make_float2(own[ND - 1][0], own[ND - 1][1]));
+                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
+                  q = __ffma2_rn(dy, dy, q);
+                } else {
+                  q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
+                }
+                q = __ffma2_rn(dx, dx, q);
+                mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+              }
+            } else {
+              const float* obase = sObs + ((size_t)kg * MP + o0) * ND2;
+#pragma unroll 4
+              for (int o = 0; o < oc; ++o) {
+                const float4 v = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2);
+                const float th = sObsThr[o0 + o];
+                const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+                const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+                float2 q = __ffma2_rn(dy, dy, make_float2(-th, -th));
+                q = __ffma2_rn(dx, dx, q);
+                if (ND == 3) {
+                  const float kp = sObsThr[MP + o0 + o];
+                  const float4 v2 = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2 + 4);
+                  const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(kp, kp)), dz, q);
+                }
+                mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+              }
+            }
+            mask = __brev(mm) >> (32 - oc);
+          } else {
+            const int ov = max(0, min(32, m - o0));
+            mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
+          }
+          if (!live) mask = 0u;
+#ifdef SFB_EXP_NOEXACT
+          if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
+#endif
+          if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
+          // exact rows of the flagged obstacles; static and moving obstacles in separate loops so  // @stage B_obs_exact
+          // the static path issues no (speculative) global load of the track
+          auto obs_rows = [&](auto is_static) {
+            constexpr bool ST = decltype(is_static)::value;
+            while (mask) {
+              const int o = o0 + __ffs(mask) - 1;
+              mask &= mask - 1u;
+              const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                if (kk < nsteps) {
+                  const int k = 2 * kg + kk;
+                  double d[ND], r[ND];
+#pragma unroll
+                  for (int a = 0; a < ND; ++a)
+                    d[a] = p[a][kk] - (ST ? sObsC[o * ND + a] : __ldg(opos + ((size_t)a * m + o) * K1 + k));
+                  ++c_exact;
+                  if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
+                    ++c_active;
+                    double rr = 0.0;
+#pragma unroll
+                    for (int a = 0; a < ND; ++a) {
+                      g[a][kk] += r[a];
+                      rr = fma(r[a], r[a], rr);
+                    }
+                    s1 += rr;
+                  }
+                }
+              }
+            }
+          };
+          if (P.obs_static) obs_rows(std::true_type{});
+          else obs_rows(std::false_type{});
+        }
+
       }
 
       SFB_TSUB(9);
-      // B": workspace box rows (exact, every step)
+      // B": workspace box rows (exact). Compact mode first tests the FP32 positions against
+      // the box shrunk by bmg (>> their rounding error below plim): a warp whose positions are
+      // all strictly inside skips the rows, which are then exactly zero.
+      bool box_rows = true;
+      if (compact && !force) {
+        bool out = false;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+          for (int a = 0; a < ND; ++a)
+            if (kk < nsteps) out |= !(own[a][kk] <= bhi_f[a] && own[a][kk] >= blo_f[a]);
+        box_rows = __any_sync(FULL, out);
+      }  // @stage box
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        if (kk < nsteps) {
+        if (box_rows && kk < nsteps) {
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
             const double up = p[a][kk] - box_hi[a];
@@ -720,7 +817,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
       }
 
-      // C: contraction with W^T into the lane's partial G
+      // C: contraction with W^T into the lane's partial G  // @stage C_contract
       if (__any_sync(FULL, nsteps > 0)) {
 #pragma unroll
         for (int c = 0; c < NXI; ++c) {
@@ -740,7 +837,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       SFB_TSUB(10);
     }
 
-    // -------------------------------------------- reductions
+    // -------------------------------------------- reductions  // @stage G_reduce
     if (!BIG && GREG) {
 #pragma unroll
       for (int a = 0; a < (GREG ? ND : 1); ++a)
@@ -807,7 +904,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
 
     SFB_TMARK(2);
-    // -------------------------------------------- D: residuals, trace, convergence
+    // -------------------------------------------- D: residuals, trace, convergence  // @stage D_decision
     double S1 = 0.0, S2 = 0.0, FP = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
@@ -908,7 +1005,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
 
     SFB_TMARK(3);
-    // -------------------------------------------- E: multiplier update and KKT step
+    // -------------------------------------------- E: multiplier update and KKT step  // @stage E1_kkt
     // E1: one warp per column, lanes = robots. Columns (a, c): lambda+, Delta and the robot
     // sum of Delta; columns (a, r): u = b - E xi, its robot sum, and max|u| (the boundary
     // residual of the xi committed at it-1, solver.py:336-337). Sums use a fixed xor tree.
@@ -976,7 +1073,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         for (int w = 0; w < NW; ++w)
           if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
     }
-    // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp
+    // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp  // @stage E2_kkt
     for (int col = warp; col < ncolD; col += nw) {
       const int a = col / NXI, c = col - a * NXI;
       double m0 = 0.0, m1 = 0.0;
@@ -1016,7 +1113,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     __syncthreads();
     SFB_TMARK(5);
   }
-#ifdef SFB_PHASE_TIMING
+#ifdef SFB_PHASE_TIMING  // @stage epilogue
   if (tid == 0 && P.counters) {
     for (int q = 0; q < 14; ++q) P.counters[(size_t)b * 20 + 4 + q] = (unsigned long long)t_ph[q];
   }
