@@ -102,6 +102,10 @@ struct ConstOff {
 // number of 16-B units, so 8 lanes loading 8 different rows hit 8 different bank groups
 __host__ __device__ constexpr int nxi_pad(int nxi) { return ((nxi + 1) & ~1) % 4 == 0 ? ((nxi + 1) & ~1) + 2 : ((nxi + 1) & ~1); }
 
+// row stride (doubles) of the g table: >= cols and 8 mod 16, so the 4 k-rows of a DMMA
+// B fragment (8 consecutive columns each) fall into disjoint bank halves
+__host__ __device__ constexpr int tab_stride(int cols) { return ((cols + 15) & ~15) + 8; }
+
 __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
 
 // append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
@@ -201,7 +205,7 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 #endif
 
 #ifndef SFB_GREG
-#define SFB_GREG 0   // n <= 32: G partials in registers (1) or per-lane shared-memory slots (0)
+#define SFB_GREG 0   // n <= 32: axes of the G partials held in registers (the rest in per-lane smem slots)
 #endif
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
@@ -253,7 +257,14 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots (BIG)
   // n <= 32: per-lane G partials [nw][NXI][ND][32] (conflict-free, lane-contiguous)
   double* sGl = reinterpret_cast<double*>(smem + P.L.gl);
-  // KKT scratch (aliases the union region (BIG) / the per-lane partials after the reduction)
+  // TBL (one k-group row of 32 robots per warp task): g_i(k) goes to a [k][axis * n + i] table
+  // (row stride TS = 8 mod 16 doubles: conflict-free DMMA fragment loads) for the
+  // tensor-core contraction, instead of per-lane partials of G
+  constexpr bool TBL = !BIG && NJ == 32;
+  double* sTab = sGl;
+  const int TS = tab_stride(ND * n);
+  // KKT scratch (aliases the union region (BIG) / the per-lane partials or g table after the
+  // reduction; TBL rows it overwrites are rewritten by their task, or masked, before use)
   double* sD = reinterpret_cast<double*>(BIG ? uni : smem + P.L.gl);  // [ND*n][NXI]
   double* sU = sD + nv;                                             // [ND*n][NB]
   double* sSD = sU + ND * n * NB;                                   // [ND][NXI]
@@ -465,17 +476,18 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 
   for (int it = 0;; ++it) {  // @stage iter_top
     // -------------------------------------------- A/B/C per k-group task
-    constexpr bool GREG = BIG || SFB_GREG;   // partials held in registers
-    double Gp[GREG ? ND : 1][GREG ? NXI : 1];
+    // G partials (not TBL): the first RA axes in registers, the rest in per-lane smem slots
+    constexpr int RA = BIG ? ND : (SFB_GREG > ND ? ND : SFB_GREG);
+    double Gp[RA > 0 ? RA : 1][NXI];
     double* gl = sGl + (size_t)warp * NXI * ND * 32 + lane;          // this lane's partials, stride 32
-    if (GREG) {
+    if (!TBL) {
 #pragma unroll
-      for (int a = 0; a < (GREG ? ND : 1); ++a)
+      for (int a = 0; a < ND; ++a)
 #pragma unroll
-        for (int c = 0; c < (GREG ? NXI : 1); ++c) Gp[a][c] = 0.0;
-    } else {
-#pragma unroll
-      for (int q = 0; q < NXI * ND; ++q) gl[q * 32] = 0.0;
+        for (int c = 0; c < NXI; ++c) {
+          if (a < RA) Gp[a < RA ? a : 0][c] = 0.0;
+          else gl[(c * ND + a) * 32] = 0.0;
+        }
     }
     float* posw = sPos + (size_t)(warp * SUB + sub) * NJ * ND2;        // !BIG: this k-group's row
     double s1 = 0.0, s2 = 0.0;
@@ -817,15 +829,25 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
       }
 
-      // C: contraction with W^T into the lane's partial G  // @stage C_contract
-      if (__any_sync(FULL, nsteps > 0)) {
+      // C: TBL stores g_i(k) for the tensor-core contraction after the task loop; otherwise
+      // contraction with W^T into the lane's partial G  // @stage C_contract
+      if (TBL) {
+        if (live) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            if (kk < nsteps)
+#pragma unroll
+              for (int a = 0; a < ND; ++a) sTab[(size_t)(2 * kg + kk) * TS + a * n + i] = g[a][kk];
+        }
+      } else if (__any_sync(FULL, nsteps > 0)) {
 #pragma unroll
         for (int c = 0; c < NXI; ++c) {
           const double2 w = wk2[c];
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
-            if (GREG) {
-              Gp[GREG ? a : 0][GREG ? c : 0] = fma(w.x, g[a][0], fma(w.y, g[a][1], Gp[GREG ? a : 0][GREG ? c : 0]));
+            if (a < RA) {
+              double& acc = Gp[a < RA ? a : 0][c];
+              acc = fma(w.x, g[a][0], fma(w.y, g[a][1], acc));
             } else {
               double* q = gl + (c * ND + a) * 32;
               *q = fma(w.x, g[a][0], fma(w.y, g[a][1], *q));
@@ -838,11 +860,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     }
 
     // -------------------------------------------- reductions  // @stage G_reduce
-    if (!BIG && GREG) {
+    if (!BIG && RA > 0) {
 #pragma unroll
-      for (int a = 0; a < (GREG ? ND : 1); ++a)
+      for (int a = 0; a < (RA > 0 ? RA : 1); ++a)
 #pragma unroll
-        for (int c = 0; c < (GREG ? NXI : 1); ++c) gl[(c * ND + a) * 32] = Gp[a][c];
+        for (int c = 0; c < NXI; ++c) gl[(c * ND + a) * 32] = Gp[a][c];
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -857,7 +879,49 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     __syncthreads();   // all positions consumed: the union region is free
     SFB_TMARK(1);
 
-    if (!BIG) {
+    if (TBL) {
+      // G^T (c x col) = W^T (c x k) . g (k x col) on the FP64 tensor cores (DMMA m8n8k4): warp
+      // per 8-column tile, two 8-row tiles of c, k in steps of 4 over this CTA's steps [klo, khi)
+      // (rows outside are masked, never read), even/odd k-steps in separate accumulators then
+      // added: a fixed order, deterministic. A(m = c, k) = W[k][c], B(k, col) = g[k][col].
+      const int ncol = ND * n, ntl = (ncol + 7) >> 3;
+      const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
+      const int rq = lane >> 2, kq = lane & 3;
+      for (int tl = warp; tl < ntl; tl += nw) {
+        double acc[2][2][2];   // [parity][m tile][2]
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) acc[q2][mt][0] = acc[q2][mt][1] = 0.0;
+        const int colB = tl * 8 + rq;
+        const bool colok = colB < ncol;
+        for (int ks = klo >> 2; ks < (khi + 3) >> 2; ks += 2) {
+#pragma unroll
+          for (int q2 = 0; q2 < 2; ++q2) {
+            const int k = 4 * (ks + q2) + kq;
+            const bool kin = k >= klo && k < khi;
+            const double bv = (kin && colok) ? sTab[(size_t)k * TS + colB] : 0.0;
+            const double* wk = sW + ((size_t)(k >> 1) * NXI) * 2 + (k & 1);
+            const double a0 = (kin && rq < NXI) ? wk[rq * 2] : 0.0;
+            const double a1 = (kin && 8 + rq < NXI) ? wk[(8 + rq) * 2] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[q2][0][0]), "+d"(acc[q2][0][1]) : "d"(a0), "d"(bv));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[q2][1][0]), "+d"(acc[q2][1][1]) : "d"(a1), "d"(bv));
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int c = mt * 8 + rq;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = tl * 8 + kq * 2 + j;
+            if (c < NXI && col < ncol) sG[col * NXI + c] = acc[0][mt][j] + acc[1][mt][j];
+          }
+        }
+      }
+      __syncthreads();
+    } else if (!BIG) {
       // G = sum over warps, then over the k-group sub-lanes, of the per-lane partials (fixed order)
       // thread = (column (c, a), robot): consecutive threads read consecutive lanes
       for (int o = tid; o < NXI * ND * 32; o += nt) {

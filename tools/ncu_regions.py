@@ -47,28 +47,35 @@ def main():
             continue
         addr = r[2]
         try:
-            insts.append((int(addr, 16), cur_file, cur_line, int(r[7] or 0), int(r[6] or 0)))
+            wf = int(r[hdr.index("L1 Wavefronts Shared")] or 0)
+            wi = int(r[hdr.index("L1 Wavefronts Shared Ideal")] or 0)
+            insts.append((int(addr, 16), cur_file, cur_line, int(r[7] or 0), int(r[6] or 0), wf, wi))
         except ValueError:
             pass
     insts.sort()
     lines_sorted = [m[0] for m in marks]
     agg = {}
     last_stage = "prologue"
-    for addr, f, line, ex, sm in insts:
+    for addr, f, line, ex, sm, wf, wi in insts:
         if f and f.endswith(kfile) and line is not None:
             k = bisect.bisect_right(lines_sorted, line) - 1
             last_stage = marks[k][1] if k >= 0 else "prologue"
-        e = agg.setdefault(last_stage, [0, 0])
+        e = agg.setdefault(last_stage, [0, 0, 0, 0])
         e[0] += ex
         e[1] += sm
+        e[2] += wf
+        e[3] += wi
     te = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[1] for v in agg.values()) or 1
-    print(f"{'stage':24s} {'instr %':>8s} {'stall %':>8s}   warp-instr")
+    tw = sum(v[2] for v in agg.values()) or 1
+    print(f"{'stage':24s} {'instr %':>8s} {'stall %':>8s} {'smem wf %':>9s} {'wf/ideal':>8s}   warp-instr")
     order = [m[1] for m in marks]
     for name in ["prologue"] + order:
         if name in agg:
-            e, s = agg.pop(name)
-            print(f"{name:24s} {100 * e / te:8.1f} {100 * s / ts:8.1f}   {e:,}")
+            e, s, w, wi = agg.pop(name)
+            print(f"{name:24s} {100 * e / te:8.1f} {100 * s / ts:8.1f} {100 * w / tw:9.1f} "
+                  f"{(w / wi if wi else 0):8.2f}   {e:,}")
+    print(f"total shared-memory wavefronts {tw:,}")
 
 
 if __name__ == "__main__":
