@@ -102,9 +102,14 @@ struct ConstOff {
 // number of 16-B units, so 8 lanes loading 8 different rows hit 8 different bank groups
 __host__ __device__ constexpr int nxi_pad(int nxi) { return ((nxi + 1) & ~1) % 4 == 0 ? ((nxi + 1) & ~1) + 2 : ((nxi + 1) & ~1); }
 
-// row stride (doubles) of the g table: >= cols and 8 mod 16, so the 4 k-rows of a DMMA
-// B fragment (8 consecutive columns each) fall into disjoint bank halves
-__host__ __device__ constexpr int tab_stride(int cols) { return ((cols + 15) & ~15) + 8; }
+// row stride (doubles) of the g table: >= cols and 4 mod 16, so a half-warp's DMMA B fragment
+// load (4 k-rows x 4 consecutive columns) hits 16 distinct bank pairs
+__host__ __device__ constexpr int tab_stride(int cols) { return ((cols + 15) & ~15) + 4; }
+// W in shared memory: rows of WSTR = 12 doubles (n_basis <= 12, zero padded), all 2 * NKG
+// steps rounded up to 4. Rows 96 B apart: the 4 k-rows x 4 columns of a half-warp's DMMA A
+// fragment load hit 16 distinct bank pairs, and a task's two step rows load as double2 pairs.
+constexpr int WSTR = 12;
+__host__ __device__ constexpr int w_rows(int nkg) { return (2 * nkg + 3) & ~3; }
 
 __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
 
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   double* sXi = reinterpret_cast<double*>(smem + P.L.xi);    // [ND*n][NXP]
   double* sLam = reinterpret_cast<double*>(smem + P.L.lam);  // [ND*n][NXP]
   double* sTgt = reinterpret_cast<double*>(smem + P.L.tgt);  // [ND*n][NXI] (projection target)
-  double* sW = reinterpret_cast<double*>(smem + P.L.w);      // [NKG][NXI][2]
+  double* sW = reinterpret_cast<double*>(smem + P.L.w);      // [w_rows(NKG)][WSTR], zero padded
   double* sE = reinterpret_cast<double*>(smem + P.L.e);      // [NB][NXI]
   double* sQ = reinterpret_cast<double*>(smem + P.L.q);      // [NXI][NXI]
   double* sPxx = reinterpret_cast<double*>(smem + P.L.pxx);
@@ -280,10 +285,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   };
 
   // ------------------------------------------------------------------ setup
-  for (int idx = tid; idx < NKG * NXI * 2; idx += nt) {
-    const int kg = idx / (NXI * 2), rem = idx - kg * NXI * 2, c = rem >> 1, kk = rem & 1;
-    const int k = 2 * kg + kk;
-    sW[idx] = (k < K1) ? P.consts[co.W + k * NXI + c] : 0.0;
+  for (int idx = tid; idx < w_rows(NKG) * WSTR; idx += nt) {
+    const int k = idx / WSTR, c = idx - k * WSTR;
+    sW[idx] = (k < K1 && c < NXI) ? P.consts[co.W + k * NXI + c] : 0.0;
   }
   for (int idx = tid; idx < NB * NXI; idx += nt) sE[idx] = P.consts[co.E + idx];
   for (int idx = tid; idx < NXI * NXI; idx += nt) {
@@ -498,7 +502,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       const int kg = kg_ok ? kg_raw : NKG - 1;
       const bool live = robot_ok && kg_ok;
       const bool has1 = 2 * kg + 1 < K1;
-      const double2* wk2 = reinterpret_cast<const double2*>(sW + (size_t)kg * NXI * 2);
+      const double* w0r = sW + (size_t)(2 * kg) * WSTR;   // W rows of the two steps
+      const double* w1r = w0r + WSTR;
 #ifdef SFB_PHASE_TIMING
       if (tid == 0) t_sub = clock64();
 #endif
@@ -509,21 +514,22 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       for (int a = 0; a < ND; ++a) p[a][0] = p[a][1] = 0.0;
 #pragma unroll
       for (int c = 0; c + 1 < NXI; c += 2) {
-        const double2 w0 = wk2[c], w1 = wk2[c + 1];
+        const double2 u0 = *reinterpret_cast<const double2*>(w0r + c);
+        const double2 u1 = *reinterpret_cast<const double2*>(w1r + c);
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
           const double2 x = *reinterpret_cast<const double2*>(xrow + a * n * NXP + c);
-          p[a][0] = fma(w1.x, x.y, fma(w0.x, x.x, p[a][0]));
-          p[a][1] = fma(w1.y, x.y, fma(w0.y, x.x, p[a][1]));
+          p[a][0] = fma(u0.y, x.y, fma(u0.x, x.x, p[a][0]));
+          p[a][1] = fma(u1.y, x.y, fma(u1.x, x.x, p[a][1]));
         }
       }
       if (NXI & 1) {
-        const double2 w0 = wk2[NXI - 1];
+        const double u0 = w0r[NXI - 1], u1 = w1r[NXI - 1];
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
           const double x = xrow[a * n * NXP + NXI - 1];
-          p[a][0] = fma(w0.x, x, p[a][0]);
-          p[a][1] = fma(w0.y, x, p[a][1]);
+          p[a][0] = fma(u0, x, p[a][0]);
+          p[a][1] = fma(u1, x, p[a][1]);
         }
       }
       float own[ND][2];
@@ -842,7 +848,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       } else if (__any_sync(FULL, nsteps > 0)) {
 #pragma unroll
         for (int c = 0; c < NXI; ++c) {
-          const double2 w = wk2[c];
+          const double2 w = make_double2(w0r[c], w1r[c]);
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
             if (a < RA) {
@@ -901,9 +907,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
             const int k = 4 * (ks + q2) + kq;
             const bool kin = k >= klo && k < khi;
             const double bv = (kin && colok) ? sTab[(size_t)k * TS + colB] : 0.0;
-            const double* wk = sW + ((size_t)(k >> 1) * NXI) * 2 + (k & 1);
-            const double a0 = (kin && rq < NXI) ? wk[rq * 2] : 0.0;
-            const double a1 = (kin && 8 + rq < NXI) ? wk[(8 + rq) * 2] : 0.0;
+            const double* wk = sW + (size_t)k * WSTR;      // zero padded beyond NXI
+            const double a0 = kin ? wk[rq] : 0.0;
+            const double a1 = (kin && 8 + rq < NXI) ? wk[8 + rq] : 0.0;
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                          : "+d"(acc[q2][0][0]), "+d"(acc[q2][0][1]) : "d"(a0), "d"(bv));
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
