@@ -1143,7 +1143,74 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         for (int w = 0; w < NW; ++w)
           if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
     }
-    // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u), column per warp  // @stage E2_kkt
+    // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u)  // @stage E2_kkt
+    if (TBL) {
+      // on the FP64 tensor cores: X+ (rows x c) = (X + mean) + [Delta | u] (rows x (NXI + NB))
+      // . [Pxx | Pxb]^T, warp per 8-row tile, two 8-column tiles, k in steps of 4 (DMMA m8n8k4).
+      // mean[a][c] is computed by lane a * NXI + c (and + 32) and fetched by shuffle.
+      const int KT = NXI + NB, nrow = ND * n, nmt = (nrow + 7) >> 3;
+      const int rq = lane >> 2, kq = lane & 3;
+      double mv[(ND * NXI + 31) / 32];
+#pragma unroll
+      for (int h = 0; h < (ND * NXI + 31) / 32; ++h) {
+        const int idx = lane + 32 * h;
+        double m0 = 0.0, m1 = 0.0;
+        if (idx < ND * NXI) {
+          const int a = idx / NXI, c = idx - a * NXI;
+#pragma unroll
+          for (int c2 = 0; c2 < NXI; ++c2) m0 = fma(sDxx[c * NXI + c2], sSD[a * NXI + c2], m0);
+#pragma unroll
+          for (int r = 0; r < NBM; ++r)
+            if (r < NB) m1 = fma(sDxb[c * NB + r], sSU[a * NB + r], m1);
+        }
+        mv[h] = m0 + m1;
+      }
+      for (int tl = warp; tl < nmt; tl += nw) {
+        const int row = tl * 8 + rq;
+        const bool rowok = row < nrow;
+        const int ra = (row >= n) + (ND == 3 && row >= 2 * n);
+        double acc[2][2];
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = nt2 * 8 + 2 * kq + j;
+            const int idx = ra * NXI + c;
+            double mval = 0.0;
+#pragma unroll
+            for (int h = 0; h < (ND * NXI + 31) / 32; ++h) {
+              const double v = __shfl_sync(FULL, mv[h], idx & 31);
+              if ((idx >> 5) == h) mval = v;
+            }
+            acc[nt2][j] = (rowok && c < NXI) ? sXi[row * NXP + c] + mval : 0.0;
+          }
+        for (int ks = 0; ks < (KT + 3) >> 2; ++ks) {
+          const int k = 4 * ks + kq;
+          double av = 0.0;
+          if (rowok) av = (k < NXI) ? sD[row * NXI + k] : ((k < KT) ? sU[row * NB + (k - NXI)] : 0.0);
+#pragma unroll
+          for (int nt2 = 0; nt2 < 2; ++nt2) {
+            const int c = nt2 * 8 + rq;
+            const double bv = (c < NXI && k < KT) ? ((k < NXI) ? sPxx[c * NXI + k] : sPxb[c * NB + (k - NXI)]) : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[nt2][0]), "+d"(acc[nt2][1]) : "d"(av), "d"(bv));
+          }
+        }
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = nt2 * 8 + 2 * kq + j;
+            if (rowok && c < NXI) {
+              const double xo = sXi[row * NXP + c];
+              const double xn = acc[nt2][j];
+              sXi[row * NXP + c] = xn;
+              const double dx = xn - xo;
+              fpp = fma(dx, dx, fpp);
+            }
+          }
+      }
+    } else
     for (int col = warp; col < ncolD; col += nw) {
       const int a = col / NXI, c = col - a * NXI;
       double m0 = 0.0, m1 = 0.0;
