@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     const int k = idx / WSTR, c = idx - k * WSTR;
     sW[idx] = (k < K1 && c < NXI) ? P.consts[co.W + k * NXI + c] : 0.0;
   }
+  if (TBL) {   // g-table rows K1 .. (K1 rounded up to 4) are read by the contraction, never written
+    for (int idx = tid; idx < (((K1 + 3) & ~3) - K1) * TS; idx += nt) sTab[(size_t)K1 * TS + idx] = 0.0;
+  }
   for (int idx = tid; idx < NB * NXI; idx += nt) sE[idx] = P.consts[co.E + idx];
   for (int idx = tid; idx < NXI * NXI; idx += nt) {
     sQ[idx] = P.consts[co.Q + idx];
@@ -901,6 +904,33 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           for (int mt = 0; mt < 2; ++mt) acc[q2][mt][0] = acc[q2][mt][1] = 0.0;
         const int colB = tl * 8 + rq;
         const bool colok = colB < ncol;
+        if (klo == 0 && khi == K1) {
+          // whole time axis: rows K1.. of the table and of W are zero, columns beyond the live
+          // ones only feed output rows/columns that are not stored: no masks
+          const double* tb = sTab + (size_t)kq * TS + colB;
+          const double* wa = sW + (size_t)kq * WSTR + rq;
+          const int nks = (K1 + 3) >> 2;
+          int ks = 0;
+          for (; ks + 1 < nks; ks += 2) {
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) {
+              const double bv = tb[(size_t)(4 * (ks + q2)) * TS];
+              const double a0 = wa[(size_t)(4 * (ks + q2)) * WSTR], a1 = wa[(size_t)(4 * (ks + q2)) * WSTR + 8];
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(acc[q2][0][0]), "+d"(acc[q2][0][1]) : "d"(a0), "d"(bv));
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(acc[q2][1][0]), "+d"(acc[q2][1][1]) : "d"(a1), "d"(bv));
+            }
+          }
+          if (ks < nks) {
+            const double bv = tb[(size_t)(4 * ks) * TS];
+            const double a0 = wa[(size_t)(4 * ks) * WSTR], a1 = wa[(size_t)(4 * ks) * WSTR + 8];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[0][0][0]), "+d"(acc[0][0][1]) : "d"(a0), "d"(bv));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[0][1][0]), "+d"(acc[0][1][1]) : "d"(a1), "d"(bv));
+          }
+        } else
         for (int ks = klo >> 2; ks < (khi + 3) >> 2; ks += 2) {
 #pragma unroll
           for (int q2 = 0; q2 < 2; ++q2) {
