@@ -619,6 +619,11 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       };
 
       {
+        // n <= 32 with static obstacles (one chunk): the exact pair and obstacle rows run in one
+        // loop, a lane's pair bits first then its obstacle bits — each lane's order of the
+        // two-loop form, in max(pairs + obstacles) instead of max(pairs) + max(obstacles) steps
+        const bool merge = !BIG && P.obs_static && m > 0 && MP <= 32;
+        unsigned pdef = 0u;
         // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
         for (int j0 = 0; j0 < (BIG ? n : 1); j0 += 32) {
           const int jc = BIG ? min(32, n - j0) : n;
@@ -637,6 +642,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
           SFB_TSUB(7);
 
           // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)  // @stage B_pair_exact
+          if (merge) pdef = mask;
+          else
           while (__any_sync(FULL, mask != 0u)) {
             const bool act = mask != 0u;
             const int jl = act ? __ffs(mask) - 1 : 0;
@@ -805,8 +812,66 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
               }
             }
           };
-          if (P.obs_static) obs_rows(std::true_type{});
-          else obs_rows(std::false_type{});
+          if (merge) {
+            unsigned pmk = pdef, omk = mask;
+            while (__any_sync(FULL, (pmk | omk) != 0u)) {
+              const bool isp = pmk != 0u;
+              const bool act = isp || omk != 0u;
+              int jl = 0, o = 0;
+              if (isp) {
+                jl = __ffs(pmk) - 1;
+                pmk &= pmk - 1u;
+              } else if (act) {
+                o = __ffs(omk) - 1;
+                omk &= omk - 1u;
+              }
+              double pj[ND][2];
+              const int src = sub * LW + jl;
+#pragma unroll
+              for (int a = 0; a < ND; ++a)
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+              if (act) {
+                double ia2 = r_inv_a2, ib2 = r_inv_b2, aa = ra, bb = rb_ax, cs = (i < jl) ? 1.0 : -1.0;
+                if (!isp) {
+                  const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
+                  ia2 = ax.x;
+                  ib2 = ax.y;
+                  aa = ax.z;
+                  bb = ax.w;
+                  cs = 1.0;
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
+                }
+                const bool once = !isp || i < jl;   // rows the reference's F holds once
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                  if (kk < nsteps) {
+                    double d[ND], r[ND];
+#pragma unroll
+                    for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
+                    ++c_exact;
+                    if (row_exact<ND>(d, ia2, ib2, aa, bb, d_max, cs, r)) {
+                      double rr = 0.0;
+#pragma unroll
+                      for (int a = 0; a < ND; ++a) {
+                        g[a][kk] += r[a];
+                        rr = fma(r[a], r[a], rr);
+                      }
+                      if (once) {
+                        ++c_active;
+                        s1 += rr;
+                      }
+                    }
+                  }
+                }
+              }
+            }
+          } else if (P.obs_static) {
+            obs_rows(std::true_type{});
+          } else {
+            obs_rows(std::false_type{});
+          }
         }
 
       }
