@@ -124,6 +124,13 @@ __device__ __forceinline__ double rsqrt_fast(double q) {
   return y * fma(-0.5 * q, y * y, 1.5);
 }
 
+// the same for q in (0, 1): only underflow of the FP32 seed needs the slow path
+__device__ __forceinline__ double rsqrt_fast01(double q) {
+  if (!(q > 1e-30)) return rsqrt(q);
+  const double y = (double)rsqrtf((float)q);
+  return y * fma(-0.5 * q, y * y, 1.5);
+}
+
 // Exact FP64 residual of one separation row (constraints.py:166-247, trig-free):
 // r1 = delta * (1 - clip(rho, 1, d_max) / rho), coincident rows use alpha = 0, beta = pi/2.
 template <int ND>
@@ -140,7 +147,7 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
       if (ND == 3) r[ND - 1] = -ax_b * COS_HALF_PI * coinc_sign;
       return true;
     }
-    f = 1.0 - rsqrt_fast(q);
+    f = 1.0 - rsqrt_fast01(q);
   } else if (q > d_max * d_max) {
     f = 1.0 - d_max * rsqrt(q);
   } else {
@@ -479,7 +486,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   double eq_max = 0.0;
-  unsigned long long c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
+  // per-thread counts fit 32 bits (rows of one lane over one solve); summed in 64 bits at the end
+  unsigned c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
   for (int it = 0;; ++it) {  // @stage iter_top
     // -------------------------------------------- A/B/C per k-group task
@@ -638,7 +646,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #ifdef SFB_EXP_NOEXACT
           if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;   // timing ablation only
 #endif
-          if (P.counters) c_screen += (unsigned long long)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
+          if (P.counters) c_screen += (unsigned)(jc - ((i >= j0 && i < j0 + jc) ? 1 : 0)) * nsteps;
           SFB_TSUB(7);
 
           // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)  // @stage B_pair_exact
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #ifdef SFB_EXP_NOEXACT
           if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
 #endif
-          if (P.counters) c_screen += (unsigned long long)max(0, min(32, m - o0)) * nsteps;
+          if (P.counters) c_screen += (unsigned)max(0, min(32, m - o0)) * nsteps;
           // exact rows of the flagged obstacles; static and moving obstacles in separate loops so  // @stage B_obs_exact
           // the static path issues no (speculative) global load of the track
           auto obs_rows = [&](auto is_static) {
@@ -826,11 +834,13 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
                 omk &= omk - 1u;
               }
               double pj[ND][2];
-              const int src = sub * LW + jl;
+              if (__any_sync(FULL, isp)) {
+                const int src = sub * LW + jl;
 #pragma unroll
-              for (int a = 0; a < ND; ++a)
+                for (int a = 0; a < ND; ++a)
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+                  for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+              }
               if (act) {
                 double ia2 = r_inv_a2, ib2 = r_inv_b2, aa = ra, bb = rb_ax, cs = (i < jl) ? 1.0 : -1.0;
                 if (!isp) {
@@ -1352,11 +1362,12 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #endif
 
   if (P.counters) {
+    unsigned long long w_exact = c_exact, w_active = c_active, w_screen = c_screen;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      c_exact += __shfl_xor_sync(FULL, c_exact, off);
-      c_active += __shfl_xor_sync(FULL, c_active, off);
-      c_screen += __shfl_xor_sync(FULL, c_screen, off);
+      w_exact += __shfl_xor_sync(FULL, w_exact, off);
+      w_active += __shfl_xor_sync(FULL, w_active, off);
+      w_screen += __shfl_xor_sync(FULL, w_screen, off);
     }
     if (lane == 0) {
 #ifdef SFB_PHASE_TIMING
@@ -1364,10 +1375,10 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
 #else
       unsigned long long* cb = P.counters + (size_t)b * 4;
 #endif
-      atomicAdd(cb + 0, c_exact);
-      atomicAdd(cb + 1, c_active);
-      atomicAdd(cb + 2, c_screen);
-      if (warp == 0 && crank == 0) atomicAdd(cb + 3, c_evals);
+      atomicAdd(cb + 0, w_exact);
+      atomicAdd(cb + 1, w_active);
+      atomicAdd(cb + 2, w_screen);
+      if (warp == 0 && crank == 0) atomicAdd(cb + 3, (unsigned long long)c_evals);
     }
   }
 }
