@@ -54,7 +54,7 @@ struct Layout {       // byte offsets into dynamic shared memory
 struct KParams {
   int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
   int compact;     // n <= 32, MP <= 32: compacted exact rows + obstacle grid (static obstacles)
-  int kgs;         // n > 32: k-group rows of positions held per CTA (its time slice)
+  int kgs;         // n > 32: k-group position rows held per CTA (2 ring slots per k-group worker)
   int csize;       // CTAs per member (thread-block cluster along the time axis), 1..8
   int mode, max_iters, early_exit;
   double rho, primal_tol, fp_tol, d_max, inv_n;
@@ -221,8 +221,10 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 #endif
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
-template <int ND, int NXI, int NJ, bool BIG>
-__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
+// BIG2: the n > 32 kernel capped at 128 registers so that two CTAs share an SM (large
+// batches whose layout fits half the shared memory); BIG alone runs one CTA per SM
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
+__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
@@ -259,13 +261,15 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
   double* sObsC = reinterpret_cast<double*>(smem + P.L.obs_c);     // [MP][ND] exact centers (static)
   float* sObsS = reinterpret_cast<float*>(smem + P.L.obs_s);       // [MP][OS] static: -x -y (-z) -thr (kappa)
   float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [NKG][MP][ND2] (dynamic)
-  float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [NKG][8] (n > 32)
+  float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [kgs][8] (n > 32)
   unsigned char* uni = smem + P.L.uni;
   const int NROW = BIG ? n : NJ;                                    // bodies per k-group row
   // n > 32: positions of every k-group are shared by the robot-block warps of that k-group;
   // n <= 32: a warp holds all robots of its k-groups, so it owns a private position row
   float* sPos = reinterpret_cast<float*>(uni);                      // BIG [NKG][NROW][ND2] / [nw][32/NJ][NJ][ND2]
   float* sLo = sPos + (size_t)P.kgs * NROW * ND2;                   // [kgs][NROW][ND2] lo (BIG)
+  // n > 32: a k-group's positions live in ring slot 2 wk + (task parity) of its worker: the
+  // worker's named barrier at the next task orders all reads of a slot before its reuse
   double* sSlot = reinterpret_cast<double*>(uni);                   // G partial slots (BIG)
   // n <= 32: per-lane G partials [nw][NXI][ND][32] (conflict-free, lane-contiguous)
   double* sGl = reinterpret_cast<double*>(smem + P.L.gl);
@@ -507,7 +511,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
     float* posw = sPos + (size_t)(warp * SUB + sub) * NJ * ND2;        // !BIG: this k-group's row
     double s1 = 0.0, s2 = 0.0;
 
-    for (int ts = ts_lo + wk; ts < ts_hi; ts += nwk) {
+    for (int ts = ts_lo + wk, tcnt = 0; ts < ts_hi; ts += nwk, ++tcnt) {
+      const int pslot = BIG ? 2 * wk + (tcnt & 1) : 0;
       const int kg_raw = ts * SUB + sub;
       const bool kg_ok = kg_raw < NKG;
       const int kg = kg_ok ? kg_raw : NKG - 1;
@@ -559,7 +564,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
         }
         if (ND == 3) hv[6] = hv[7] = 0.f;
         if (BIG ? (kg_ok && robot_ok) : true) {
-          float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + i) * ND2 : posw + i * ND2);
+          float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)pslot * NROW + i) * ND2 : posw + i * ND2);
           dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
           if (BIG) {
@@ -570,7 +575,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
               lv[2 * a + 1] = has1 ? (float)(p[a][1] - (double)hv[2 * a + 1]) : 0.f;
             }
             if (ND == 3) lv[6] = lv[7] = 0.f;
-            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)(kg - ts_lo) * NROW + i) * ND2);
+            float4* dl = reinterpret_cast<float4*>(sLo + ((size_t)pslot * NROW + i) * ND2);
             dl[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
             if (ND == 3) dl[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
           }
@@ -578,10 +583,10 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       }
       pabs = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(pabs)));
       if (BIG) {
-        if (lane == 0) sPmax[(kg - ts_lo) * 8 + rbk] = pabs;
+        if (lane == 0) sPmax[pslot * 8 + rbk] = pabs;
         // every robot block of this k-group must have stored its positions
         asm volatile("bar.sync %0, %1;" ::"r"(1 + wk), "r"(P.RB * 32) : "memory");
-        for (int r = 0; r < P.RB; ++r) pabs = fmaxf(pabs, sPmax[(kg - ts_lo) * 8 + r]);
+        for (int r = 0; r < P.RB; ++r) pabs = fmaxf(pabs, sPmax[pslot * 8 + r]);
       } else {
         __syncwarp();
       }
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
       // pair screen of one chunk of 32 bodies: bit j set if body j0 + j may be within contact
       auto pair_screen = [&](int j0, int jc) -> unsigned {
         const float2 thr2 = make_float2(-r_thr, -r_thr);
-        const float* base = BIG ? sPos + ((size_t)(kg - ts_lo) * NROW + j0) * ND2 : posw;
+        const float* base = BIG ? sPos + ((size_t)pslot * NROW + j0) * ND2 : posw;
         unsigned mm = 0u;
         auto screen = [&](const float* bp) {
           const float4 v = *reinterpret_cast<const float4*>(bp);
@@ -659,8 +664,8 @@ __global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const 
             const int j = j0 + jl;
             double pj[ND][2];
             if (BIG) {
-              const float* hp = sPos + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
-              const float* lp = sLo + ((size_t)(kg - ts_lo) * NROW + (act ? j : 0)) * ND2;
+              const float* hp = sPos + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
+              const float* lp = sLo + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
 #pragma unroll
               for (int a = 0; a < ND; ++a)
 #pragma unroll

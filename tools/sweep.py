@@ -1,7 +1,7 @@
 """Throughput of the SF kernel across the BASELINE.json configs (C1-C4) and the
 robots x batch sweep (C5: 8-128 robots, batch 1-1024 instances, 20 obstacles,
 box half-width max(1, 2 sqrt(n/32)), T=100, L=500). Device-timed
-(CUDA events, inputs resident), one GPU. Writes profiles/r01_sweep.json.
+(CUDA events, inputs resident), one GPU. Writes profiles/r02_sweep.json.
 
     python tools/sweep.py [--quick]
 """
@@ -80,7 +80,7 @@ def main():
                              members=inst, L=L, seconds=t, instances_per_s=inst / t,
                              member_iters_per_s=inst * (L + 1) / t, smem_bytes=smem))
             print(json.dumps(rows[-1]), flush=True)
-    with open(os.path.join(ROOT, "profiles", "r01_sweep.json"), "w") as fh:
+    with open(os.path.join(ROOT, "profiles", "r02_sweep.json"), "w") as fh:
         json.dump({"gpu": torch.cuda.get_device_name(0), "rows": rows,
                    "note": "device-timed solve (CUDA events), inputs resident; C5 uses 20 obstacles, "
                            "box half-width max(1, 2 sqrt(n/32)), 1 sample, naive-prior warm start"},
