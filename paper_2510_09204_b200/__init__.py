@@ -12,7 +12,7 @@ from .problem import (BasisConfig, BasisMatrices, ConstraintSystem, Obstacle, Sc
 from .solver import (BatchResult, DeviceBatch, KktCache, ObjectiveMode, SolverConfig,
                      SolverResult, SolverState, batch_primal_residual, cold_start,
                      fixed_point_step, kinematic_peaks, primal_residual, rank_candidates,
-                     solve, solve_batch, solve_instances, state_from_xi, time_scale_batch,
+                     solve, solve_batch, solve_instances, solve_stream, state_from_xi, time_scale_batch,
                      time_scale_for_limits)
 from .metrics import TrajectoryMetrics, compute_metrics, dense_basis, metrics_batch
 from .pipeline import CandidateBatch, PlanResult, plan, plan_many

@@ -1254,7 +1254,10 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
     }
     // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u)  // @stage E2_kkt
-    if (TBL) {
+#ifndef SFB_E2_SIMT
+#define SFB_E2_SIMT 0   // experiments: 1 runs the SIMT xi update also on the TBL path
+#endif
+    if (TBL && !SFB_E2_SIMT) {
       // on the FP64 tensor cores: X+ (rows x c) = (X + mean) + [Delta | u] (rows x (NXI + NB))
       // . [Pxx | Pxb]^T, warp per 8-row tile, two 8-column tiles, k in steps of 4 (DMMA m8n8k4).
       // mean[a][c] is computed by lane a * NXI + c (and + 32) and fetched by shuffle.

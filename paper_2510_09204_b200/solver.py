@@ -351,7 +351,10 @@ class DeviceBatch:
 
     def __init__(self, systems, xi0, lam0=None, target=None, kind="projection", cfg=None,
                  member_instance=None, early_exit=True, trace=True, counters=False,
-                 device=None, cluster=0):
+                 device=None, cluster=0, staging=None, copy_stream=None):
+        """staging / copy_stream (solve_stream): a caller-owned pinned input arena and the
+        stream the input copies are enqueued on (asynchronously); default: the shared
+        staging buffer and synchronous copies."""
         import torch
         cfg = cfg or SolverConfig()
         if not isinstance(systems, (list, tuple)):
@@ -387,7 +390,11 @@ class DeviceBatch:
                 # xi0 and target crosses once)
                 key = (x.data_ptr(), tuple(x.shape))
                 if key not in uploaded:
-                    uploaded[key] = x.to(dev)
+                    if copy_stream is not None:
+                        with torch.cuda.stream(copy_stream):
+                            uploaded[key] = x.to(dev, non_blocking=True)
+                    else:
+                        uploaded[key] = x.to(dev)
                     direct_bytes += x.numel() * 8
                 dev_parts[name] = uploaded[key]
                 return tuple(x.shape)
@@ -430,12 +437,22 @@ class DeviceBatch:
         for name, a in host_parts:
             offs[name] = (total, a.shape)
             total += a.size
-        staging = _pinned(total)
+        if staging is None:
+            staging = _pinned(total)
+        else:                                      # caller-owned holder {"buf": pinned tensor}
+            if staging.get("buf") is None or staging["buf"].numel() < total:
+                staging["buf"] = torch.empty(max(total, 1 << 16), dtype=torch.float64).pin_memory()
+            staging = staging["buf"]
         arena_h = staging.numpy()[:total]
         for name, a in host_parts:
             o, _ = offs[name]
             arena_h[o: o + a.size] = a.reshape(-1)
-        self._in_arena = staging[:total].to(dev)       # synchronous copy from pinned memory
+        if copy_stream is not None:
+            with torch.cuda.stream(copy_stream):
+                self._in_arena = staging[:total].to(dev, non_blocking=True)
+        else:
+            self._in_arena = staging[:total].to(dev)   # synchronous copy from pinned memory
+        self.in_total = total
         self.h2d_bytes = int(arena_h.nbytes) + direct_bytes
         views = {}
         for name, (o, shp) in offs.items():
@@ -655,6 +672,81 @@ def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projectio
                        eq_violation_max=out["eq_max"], trace=out.get("trace"),
                        wall_time=time.perf_counter() - t0,
                        extra={"h2d_bytes": batch.h2d_bytes, "d2h_bytes": out["d2h_bytes"]})
+
+
+def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = None,
+                 fixed_iterations: bool = False, trace: bool = True, cluster: int = 0):
+    """Pipelined solve_instances over a sequence of batches (the serving loop): yields one
+    BatchResult per step, in order. `steps` yields (systems, xi0, lam0, target,
+    member_instance) tuples of host (or CUDA) arrays.
+
+    Every step still packs its inputs into a pinned arena, copies them to the device and
+    reads its whole output arena back; those copies run on a copy stream and the host
+    packing runs ahead, so they overlap the neighbouring steps' kernels (double-buffered
+    pinned and device arenas; step k+2 reuses step k's buffers only after step k's copies
+    completed)."""
+    import torch
+    cfg = cfg or SolverConfig()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    slots = [dict(staging=None, out=None, done=None) for _ in range(2)]
+    pending = []    # (batch, slot, d2h event, t0)
+
+    def finish(item):
+        batch, slot, ev, t0 = item
+        ev.synchronize()
+        head = slot["out"].numpy()
+        o = batch._oofs
+        B, n_d, n, n_xi = batch.out_xi.shape
+        get = lambda k: head[o[k][0]: o[k][0] + o[k][1]]
+        its = get("its").view(np.int32)[:B].copy()
+        st = get("status").view(np.int32)[:B]
+        tr = None
+        if batch.out_trace is not None:
+            T = batch.out_trace.shape[1]
+            full = get("trace").reshape(B, T, 2)
+            tr = [full[b, : its[b] + 1].copy() for b in range(B)]
+        return BatchResult(xi=get("xi").reshape(B, n_d, n, n_xi).copy(),
+                           lam=get("lam").reshape(B, n_d, n, n_xi).copy(),
+                           status=[_lib.STATUS[int(v)] for v in st], iterations=its,
+                           primal=get("primal").copy(), eq_violation_max=get("eq").copy(),
+                           trace=tr, wall_time=time.perf_counter() - t0,
+                           extra={"h2d_bytes": batch.h2d_bytes,
+                                  "d2h_bytes": int(batch._out_arena.numel()) * 8})
+
+    for k, (systems, xi0, lam0, target, mi) in enumerate(steps):
+        t0 = time.perf_counter()
+        slot = slots[k & 1]
+        if slot["done"] is not None:
+            slot["done"].synchronize()            # this slot's copies of step k-2 completed
+        if slot["staging"] is None:
+            slot["staging"] = {}
+        batch = DeviceBatch(systems, xi0, lam0, target, kind=kind, cfg=cfg, member_instance=mi,
+                            early_exit=not fixed_iterations, trace=trace, cluster=cluster,
+                            staging=slot["staging"], copy_stream=copy)
+        batch._in_arena.record_stream(compute)
+        ev_in = torch.cuda.Event()
+        ev_in.record(copy)
+        compute.wait_event(ev_in)
+        batch.launch(compute)
+        ev_k = torch.cuda.Event()
+        ev_k.record(compute)
+        nout = batch._out_arena.numel()
+        if slot["out"] is None or slot["out"].numel() < nout:
+            slot["out"] = torch.empty(nout, dtype=torch.float64).pin_memory()
+        copy.wait_event(ev_k)
+        with torch.cuda.stream(copy):
+            slot["out"][:nout].copy_(batch._out_arena, non_blocking=True)
+        batch._out_arena.record_stream(copy)
+        ev_out = torch.cuda.Event()
+        ev_out.record(copy)
+        slot["done"] = ev_out
+        pending.append((batch, dict(out=slot["out"][:nout]), ev_out, t0))
+        if len(pending) > 1:
+            yield finish(pending.pop(0))
+    while pending:
+        yield finish(pending.pop(0))
 
 
 def cold_start(scn, sys) -> SolverState:
