@@ -42,10 +42,16 @@ constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1 or dummy body) positio
 constexpr float PAD_OWN = 3.0e30f;     // padded step in the owner's registers -> never a hit
 constexpr double COS_HALF_PI = 6.123233995736766e-17;  // cos(pi/2) as the reference evaluates it
 constexpr int GRID = 32;         // obstacle candidate grid cells per axis (compact mode)
+// per-member constants kept in shared memory instead of registers (read where used, so the
+// task loop keeps its registers for the screen): doubles, then floats at KC_F
+enum { KC_INV_A2 = 0, KC_INV_B2, KC_RA, KC_RB, KC_DMAX, KC_BLO, KC_BHI = KC_BLO + 3, KC_NDBL = KC_BHI + 3 };
+enum { KC_F_BLO = 0, KC_F_BHI = 3, KC_F_GX0 = 6, KC_F_GY0, KC_F_GIX, KC_F_GIY, KC_NFLT };
+constexpr int KC_BYTES = KC_NDBL * 8 + KC_NFLT * 4;
 
 struct Layout {       // byte offsets into dynamic shared memory
   int xi, lam, tgt, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs_s, obs, pmax, gl, uni;
   int grid;           // static-obstacle candidate grid [GRID][GRID] u32 (compact mode)
+  int kc;             // per-member constants read at their (rare) use sites: KC_* below
   int xg;             // cluster exchange buffers [2][nv + 2] (set at launch when csize > 1)
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
@@ -400,7 +406,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a, so no active row is lost.
   const bool compact = !BIG && P.compact && (m == 0 || P.obs_static);
   unsigned* sGrid = reinterpret_cast<unsigned*>(smem + P.L.grid);
-  float gx0 = 0.f, gy0 = 0.f, gix = 0.f, giy = 0.f;
+  double* sKD = reinterpret_cast<double*>(smem + P.L.kc);
+  float* sKF = reinterpret_cast<float*>(sKD + KC_NDBL);
   if (compact && m > 0) {
     double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
     for (int o = 0; o < m; ++o) {
@@ -411,10 +418,12 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
       y1 = fmax(y1, sObsC[o * ND + 1] + rg);
     }
     const double hx = (x1 - x0) / GRID, hy = (y1 - y0) / GRID;
-    gx0 = (float)x0;
-    gy0 = (float)y0;
-    gix = (float)(1.0 / hx);
-    giy = (float)(1.0 / hy);
+    if (tid == 0) {
+      sKF[KC_F_GX0] = (float)x0;
+      sKF[KC_F_GY0] = (float)y0;
+      sKF[KC_F_GIX] = (float)(1.0 / hx);
+      sKF[KC_F_GIY] = (float)(1.0 / hy);
+    }
     for (int cidx = tid; cidx < GRID * GRID; cidx += nt) {
       const int cy = cidx / GRID, cx = cidx - cy * GRID;
       const double rx0 = x0 + cx * hx - 1e-3 * hx, rx1 = x0 + (cx + 1) * hx + 1e-3 * hx;
@@ -443,28 +452,30 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     cooperative_groups::this_cluster().sync();   // peers started and their barriers exist
   }
 
-  double box_lo[ND], box_hi[ND];
+  const double ra0 = P.pair_axes[(size_t)inst * 3 + 0], rb0 = P.pair_axes[(size_t)inst * 3 + 2];
+  if (tid == 0) {
 #pragma unroll
-  for (int a = 0; a < ND; ++a) {
-    box_lo[a] = P.box[((size_t)inst * 2 + 0) * ND + a];
-    box_hi[a] = P.box[((size_t)inst * 2 + 1) * ND + a];
+    for (int a = 0; a < ND; ++a) {
+      const double lo = P.box[((size_t)inst * 2 + 0) * ND + a], hi = P.box[((size_t)inst * 2 + 1) * ND + a];
+      sKD[KC_BLO + a] = lo;
+      sKD[KC_BHI + a] = hi;
+      const float bmg = 1e-4f * (1.f + (float)fmax(fabs(lo), fabs(hi)));
+      sKF[KC_F_BLO + a] = (float)lo + bmg;
+      sKF[KC_F_BHI + a] = (float)hi - bmg;
+    }
+    sKD[KC_INV_A2] = 1.0 / (ra0 * ra0);
+    sKD[KC_INV_B2] = 1.0 / (rb0 * rb0);
+    sKD[KC_RA] = ra0;
+    sKD[KC_RB] = rb0;
+    sKD[KC_DMAX] = P.d_max;
   }
-  float blo_f[ND], bhi_f[ND];
-#pragma unroll
-  for (int a = 0; a < ND; ++a) {
-    const float bmg = 1e-4f * (1.f + (float)fmax(fabs(box_lo[a]), fabs(box_hi[a])));
-    blo_f[a] = (float)box_lo[a] + bmg;
-    bhi_f[a] = (float)box_hi[a] - bmg;
-  }
-  const double ra = P.pair_axes[(size_t)inst * 3 + 0], rb_ax = P.pair_axes[(size_t)inst * 3 + 2];
-  const double r_inv_a2 = 1.0 / (ra * ra), r_inv_b2 = 1.0 / (rb_ax * rb_ax);
-  const float r_thr = (float)(ra * ra * (1.0 + 2e-3));
-  const float r_kap = (float)((ra * ra) / (rb_ax * rb_ax));
-  const double d_max = P.d_max;
+  __syncthreads();
+  const float r_thr = (float)(ra0 * ra0 * (1.0 + 2e-3));
+  const float r_kap = (float)((ra0 * ra0) / (rb0 * rb0));
   // FP32 positions carry ~2^-24 |p| error: the screen margin (1e-3 of the contact
   // distance) covers it while every |p| <= plim; beyond, rows go exact
   const float plim = P.plim * fminf(__uint_as_float(sMisc[1]),
-                                    (float)(ND == 3 ? fmin(ra, rb_ax) : ra));
+                                    (float)(ND == 3 ? fmin(ra0, rb0) : ra0));
   const double* opos = P.obs_pos + (size_t)inst * ND * m * K1;
 
   // lane -> (robot, k-group) mapping
@@ -687,7 +698,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
 #pragma unroll
                   for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
                   ++c_exact;
-                  if (row_exact<ND>(d, r_inv_a2, r_inv_b2, ra, rb_ax, d_max, cs, r)) {
+                  if (row_exact<ND>(d, sKD[KC_INV_A2], sKD[KC_INV_B2], sKD[KC_RA], sKD[KC_RB], sKD[KC_DMAX], cs, r)) {
                     if (i < j) ++c_active;   // each pair row once, like the reference's F rows
                     double rr = 0.0;
 #pragma unroll
@@ -718,7 +729,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
               // grid candidates of the lane's two positions, each confirmed by the FP32 test
               // (per lane: a robot is near few obstacles)
               auto cell = [&](float x, float y) -> unsigned {
-                const int cx = __float2int_rd((x - gx0) * gix), cy = __float2int_rd((y - gy0) * giy);
+                const int cx = __float2int_rd((x - sKF[KC_F_GX0]) * sKF[KC_F_GIX]);
+                const int cy = __float2int_rd((y - sKF[KC_F_GY0]) * sKF[KC_F_GIY]);
                 return ((unsigned)cx < (unsigned)GRID && (unsigned)cy < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
               };
               unsigned cand = live ? cell(own[0][0], own[1][0]) : 0u;
@@ -811,7 +823,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
                   for (int a = 0; a < ND; ++a)
                     d[a] = p[a][kk] - (ST ? sObsC[o * ND + a] : __ldg(opos + ((size_t)a * m + o) * K1 + k));
                   ++c_exact;
-                  if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, d_max, 1.0, r)) {
+                  if (row_exact<ND>(d, ax.x, ax.y, ax.z, ax.w, sKD[KC_DMAX], 1.0, r)) {
                     ++c_active;
                     double rr = 0.0;
 #pragma unroll
@@ -847,7 +859,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
                   for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
               }
               if (act) {
-                double ia2 = r_inv_a2, ib2 = r_inv_b2, aa = ra, bb = rb_ax, cs = (i < jl) ? 1.0 : -1.0;
+                double ia2 = sKD[KC_INV_A2], ib2 = sKD[KC_INV_B2], aa = sKD[KC_RA], bb = sKD[KC_RB];
+                double cs = (i < jl) ? 1.0 : -1.0;
                 if (!isp) {
                   const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
                   ia2 = ax.x;
@@ -866,7 +879,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
 #pragma unroll
                     for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
                     ++c_exact;
-                    if (row_exact<ND>(d, ia2, ib2, aa, bb, d_max, cs, r)) {
+                    if (row_exact<ND>(d, ia2, ib2, aa, bb, sKD[KC_DMAX], cs, r)) {
                       double rr = 0.0;
 #pragma unroll
                       for (int a = 0; a < ND; ++a) {
@@ -902,7 +915,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
         for (int kk = 0; kk < 2; ++kk)
 #pragma unroll
           for (int a = 0; a < ND; ++a)
-            if (kk < nsteps) out |= !(own[a][kk] <= bhi_f[a] && own[a][kk] >= blo_f[a]);
+            if (kk < nsteps) out |= !(own[a][kk] <= sKF[KC_F_BHI + a] && own[a][kk] >= sKF[KC_F_BLO + a]);
         box_rows = __any_sync(FULL, out);
       }  // @stage box
 #pragma unroll
@@ -910,8 +923,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
         if (box_rows && kk < nsteps) {
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
-            const double up = p[a][kk] - box_hi[a];
-            const double lo = box_lo[a] - p[a][kk];
+            const double up = p[a][kk] - sKD[KC_BHI + a];
+            const double lo = sKD[KC_BLO + a] - p[a][kk];
             if (up > 0.0) { g[a][kk] += up; s2 = fma(up, up, s2); }
             if (lo > 0.0) { g[a][kk] -= lo; s2 = fma(lo, lo, s2); }
           }
