@@ -474,8 +474,12 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   const float r_kap = (float)((ra0 * ra0) / (rb0 * rb0));
   // FP32 positions carry ~2^-24 |p| error: the screen margin (1e-3 of the contact
   // distance) covers it while every |p| <= plim; beyond, rows go exact
-  const float plim = P.plim * fminf(__uint_as_float(sMisc[1]),
-                                    (float)(ND == 3 ? fmin(ra0, rb0) : ra0));
+  // ... and rows beyond the clip (rho > d_max, constraints.py:199-201) are active too: with c the
+  // largest |coordinate| of positions and obstacle centres, every row has rho <= 2 sqrt(n_d) c /
+  // a_min, so below c = d_max a_min / (2 sqrt(n_d)) none is; above, every row goes exact
+  const float amin_all = fminf(__uint_as_float(sMisc[1]), (float)(ND == 3 ? fmin(ra0, rb0) : ra0));
+  const float plim = fminf(P.plim * amin_all,
+                           (float)(P.d_max * (1.0 - 1e-4) / (2.0 * sqrt((double)ND))) * amin_all);
   const double* opos = P.obs_pos + (size_t)inst * ND * m * K1;
 
   // lane -> (robot, k-group) mapping
