@@ -59,7 +59,7 @@ struct Layout {       // byte offsets into dynamic shared memory
 
 struct KParams {
   int n, m, MP, K1, NB, NKG, RB, obs_static, nw;
-  int compact;     // n <= 32, MP <= 32: compacted exact rows + obstacle grid (static obstacles)
+  int compact;     // n <= 32, MP <= 32: obstacle candidate grid + FP32 box prescreen (static obstacles)
   int kgs;         // n > 32: k-group position rows held per CTA (2 ring slots per k-group worker)
   int csize;       // CTAs per member (thread-block cluster along the time axis), 1..8
   int mode, max_iters, early_exit;
@@ -398,12 +398,13 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   if (obs_axmin < INFINITY) atomicMin(&sMisc[1], __float_as_uint(obs_axmin));
   __syncthreads();
   obs_absmax = __uint_as_float(sMisc[0]);
-  // compact mode (n <= 32, static obstacles): flagged rows are computed lane-parallel from a
-  // per-task entry list, and obstacle rows are nominated by a grid over the obstacles' (x, y)
-  // contact discs instead of an FP32 test of every obstacle. A cell lists obstacle o if its
-  // rectangle, widened by 1e-3 of a cell, meets the disc of radius 1.001 a_o + 1e-6 around
-  // the centre: every row the FP32 screen could flag (|p - c| < a sqrt(1 + 2e-3) with FP32
-  // positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a, so no active row is lost.
+  // compact mode (n <= 32, at most 32 static obstacles; for n > 32 the per-lane candidate loop
+  // measured slower than the broadcast screen): obstacle rows are nominated by a grid over the
+  // obstacles' (x, y) contact discs instead of an FP32 test of every obstacle. A cell lists
+  // obstacle o if its rectangle, widened by 1e-3 of a cell, meets the disc of radius
+  // 1.001 a_o + 1e-6 around the centre: every row the FP32 screen could flag (|p - c| < a
+  // sqrt(1 + 2e-3) with FP32 positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a,
+  // so no active row is lost; candidates are then confirmed by the screen's own FP32 test.
   const bool compact = !BIG && P.compact && (m == 0 || P.obs_static);
   unsigned* sGrid = reinterpret_cast<unsigned*>(smem + P.L.grid);
   double* sKD = reinterpret_cast<double*>(smem + P.L.kc);
