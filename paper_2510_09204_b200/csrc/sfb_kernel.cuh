@@ -52,6 +52,7 @@ struct Layout {       // byte offsets into dynamic shared memory
   int xi, lam, tgt, w, e, q, pxx, pxb, dxx, dxb, g, bv, red, obs_ax, obs_thr, obs_c, obs_s, obs, pmax, gl, uni;
   int grid;           // static-obstacle candidate grid [GRID][GRID] u32 (compact mode)
   int kc;             // per-member constants read at their (rare) use sites: KC_* below
+  int ub;             // TBL: boundary rows u [ND*n][NB] + their robot sums [ND][NB]
   int xg;             // cluster exchange buffers [2][nv + 2] (set at launch when csize > 1)
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
@@ -288,9 +289,11 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // KKT scratch (aliases the union region (BIG) / the per-lane partials or g table after the
   // reduction; TBL rows it overwrites are rewritten by their task, or masked, before use)
   double* sD = reinterpret_cast<double*>(BIG ? uni : smem + P.L.gl);  // [ND*n][NXI]
-  double* sU = sD + nv;                                             // [ND*n][NB]
-  double* sSD = sU + ND * n * NB;                                   // [ND][NXI]
-  double* sSU = sSD + ND * NXI;                                     // [ND][NB]
+  // TBL: the boundary rows u = b - E xi get their own buffer (the KKT scratch aliases the g
+  // table, which the task loop is still writing when the lighter warps compute u)
+  double* sU = TBL ? reinterpret_cast<double*>(smem + P.L.ub) : sD + nv;   // [ND*n][NB]
+  double* sSD = sD + nv + ND * n * NB;                              // [ND][NXI] (KKT scratch)
+  double* sSU = TBL ? sU + ND * n * NB : sSD + ND * NXI;             // [ND][NB]
 
   const ConstOff co = ConstOff::make(K1, NXI, NB);
   // (axis, robot) row of a dense index o = ai * NXI + c without runtime division
@@ -967,6 +970,36 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     }
 
     // -------------------------------------------- reductions  // @stage G_reduce
+    // TBL: the KKT's boundary-row columns u = b - E xi (xi is the iterate of this iteration
+    // and stays fixed until E2) are computed here by the warps that ran fewer k-group tasks,
+    // while the others finish theirs; E1 then only has the Delta columns
+    double equ = 0.0;
+    if (TBL) {
+      const int ncu = ND * NB, ntask = ts_hi - ts_lo, R = ntask % nw, Lw = nw - R;
+      int t0 = warp, dt = nw;                       // spread over every warp ...
+      if (R != 0 && Lw >= 4) {                      // ... or over the lighter ones
+        t0 = warp >= R ? warp - R : ncu;
+        dt = Lw;
+      }
+      for (int t = t0; t < ncu; t += dt) {
+        const int a = (t >= NB) + (ND == 3 && t >= 2 * NB), r = t - a * NB;
+        double csum = 0.0;
+        if (lane < n) {
+          const int ai = a * n + lane;
+          const double* x = sXi + ai * NXP;
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+          const double u = sBv[ai * NB + r] - v;
+          sU[ai * NB + r] = u;
+          equ = fmax(equ, fabs(u));
+          csum = u;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) csum += __shfl_xor_sync(FULL, csum, off);
+        if (lane == 0) sSU[t] = csum;
+      }
+    }
     if (!BIG && RA > 0) {
 #pragma unroll
       for (int a = 0; a < (RA > 0 ? RA : 1); ++a)
@@ -1207,8 +1240,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     // E1: one warp per column, lanes = robots. Columns (a, c): lambda+, Delta and the robot
     // sum of Delta; columns (a, r): u = b - E xi, its robot sum, and max|u| (the boundary
     // residual of the xi committed at it-1, solver.py:336-337). Sums use a fixed xor tree.
-    double fpp = 0.0, equ = 0.0;
-    const int ncolD = ND * NXI, ncol = ncolD + ND * NB;
+    double fpp = 0.0;
+    const int ncolD = ND * NXI, ncol = ncolD + (TBL ? 0 : ND * NB);
     for (int col = warp; col < ncol; col += nw) {
       double csum = 0.0;
       if (col < ncolD) {
