@@ -689,7 +689,8 @@ def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = Non
     cfg = cfg or SolverConfig()
     dev = torch.device("cuda", torch.cuda.current_device())
     compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    copy_in, copy_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)   # H2D of step k+1 must
+    # not queue behind the D2H of step k (which waits for kernel k)
     slots = [dict(staging=None, out=None, done=None) for _ in range(2)]
     pending = []    # (batch, slot, d2h event, t0)
 
@@ -724,10 +725,10 @@ def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = Non
             slot["staging"] = {}
         batch = DeviceBatch(systems, xi0, lam0, target, kind=kind, cfg=cfg, member_instance=mi,
                             early_exit=not fixed_iterations, trace=trace, cluster=cluster,
-                            staging=slot["staging"], copy_stream=copy)
+                            staging=slot["staging"], copy_stream=copy_in)
         batch._in_arena.record_stream(compute)
         ev_in = torch.cuda.Event()
-        ev_in.record(copy)
+        ev_in.record(copy_in)
         compute.wait_event(ev_in)
         batch.launch(compute)
         ev_k = torch.cuda.Event()
@@ -735,12 +736,12 @@ def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = Non
         nout = batch._out_arena.numel()
         if slot["out"] is None or slot["out"].numel() < nout:
             slot["out"] = torch.empty(nout, dtype=torch.float64).pin_memory()
-        copy.wait_event(ev_k)
-        with torch.cuda.stream(copy):
+        copy_out.wait_event(ev_k)
+        with torch.cuda.stream(copy_out):
             slot["out"][:nout].copy_(batch._out_arena, non_blocking=True)
-        batch._out_arena.record_stream(copy)
+        batch._out_arena.record_stream(copy_out)
         ev_out = torch.cuda.Event()
-        ev_out.record(copy)
+        ev_out.record(copy_out)
         slot["done"] = ev_out
         pending.append((batch, dict(out=slot["out"][:nout]), ev_out, t0))
         if len(pending) > 1:
