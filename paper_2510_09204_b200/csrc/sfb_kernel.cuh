@@ -109,9 +109,11 @@ struct ConstOff {
 // number of 16-B units, so 8 lanes loading 8 different rows hit 8 different bank groups
 __host__ __device__ constexpr int nxi_pad(int nxi) { return ((nxi + 1) & ~1) % 4 == 0 ? ((nxi + 1) & ~1) + 2 : ((nxi + 1) & ~1); }
 
-// row stride (doubles) of the g table: >= cols and 4 mod 16, so a half-warp's DMMA B fragment
-// load (4 k-rows x 4 consecutive columns) hits 16 distinct bank pairs
-__host__ __device__ constexpr int tab_stride(int cols) { return ((cols + 15) & ~15) + 4; }
+// row stride (doubles) of the g table: cols rounded up to 16; column c of row k is stored at
+// c ^ tab_swz(k), so a half-warp's DMMA B fragment load (4 k-rows x 4 consecutive columns)
+// hits 16 distinct bank pairs without row padding
+__host__ __device__ constexpr int tab_stride(int cols) { return (cols + 15) & ~15; }
+__host__ __device__ constexpr int tab_swz(int k) { return (k & 3) << 2; }
 // W in shared memory: rows of WSTR = 12 doubles (n_basis <= 12, zero padded), all 2 * NKG
 // steps rounded up to 4. Rows 96 B apart: the 4 k-rows x 4 columns of a half-warp's DMMA A
 // fragment load hit 16 distinct bank pairs, and a task's two step rows load as double2 pairs.
@@ -261,7 +263,8 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   double* sDxx = reinterpret_cast<double*>(smem + P.L.dxx);
   double* sDxb = reinterpret_cast<double*>(smem + P.L.dxb);
   double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND*n][NXI]
-  double* sBv = reinterpret_cast<double*>(smem + P.L.bv);    // [ND*n][NB]
+  // boundary values b [ND*n][NB] stay in global memory (read once per iteration, L1-resident)
+  const double* __restrict__ gBv = P.bvals + (size_t)inst * ND * n * NB;
   double* sRed = reinterpret_cast<double*>(smem + P.L.red);  // [NW][4] + misc
   double* sObsAx = reinterpret_cast<double*>(smem + P.L.obs_ax);   // [MP][4] inv_a2 inv_b2 a b
   float* sObsThr = reinterpret_cast<float*>(smem + P.L.obs_thr);   // [2][MP] thr, kappa
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // n <= 32: per-lane G partials [nw][NXI][ND][32] (conflict-free, lane-contiguous)
   double* sGl = reinterpret_cast<double*>(smem + P.L.gl);
   // TBL (one k-group row of 32 robots per warp task): g_i(k) goes to a [k][axis * n + i] table
-  // (row stride TS = 8 mod 16 doubles: conflict-free DMMA fragment loads) for the
+  // (row stride TS, XOR-swizzled columns: conflict-free DMMA fragment loads) for the
   // tensor-core contraction, instead of per-lane partials of G
   constexpr bool TBL = !BIG && NJ == 32;
   double* sTab = sGl;
@@ -332,8 +335,6 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
       sLam[ai * NXP + c] = l0[o];
       sTgt[o] = t0 ? t0[o] : 0.0;
     }
-    const double* bv = P.bvals + (size_t)inst * ND * n * NB;
-    for (int idx = tid; idx < ND * n * NB; idx += nt) sBv[idx] = bv[idx];
   }
   // obstacles, padded to MP (multiple of 4) with far-away dummies that never screen in
   for (int o = tid; o < MP; o += nt) {
@@ -947,7 +948,10 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           for (int kk = 0; kk < 2; ++kk)
             if (kk < nsteps)
 #pragma unroll
-              for (int a = 0; a < ND; ++a) sTab[(size_t)(2 * kg + kk) * TS + a * n + i] = g[a][kk];
+              for (int a = 0; a < ND; ++a) {
+                const int k = 2 * kg + kk;
+                sTab[(size_t)k * TS + ((a * n + i) ^ tab_swz(k))] = g[a][kk];
+              }
         }
       } else if (__any_sync(FULL, nsteps > 0)) {
 #pragma unroll
@@ -990,7 +994,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           double v = 0.0;
 #pragma unroll
           for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-          const double u = sBv[ai * NB + r] - v;
+          const double u = __ldg(gBv + ai * NB + r) - v;
           sU[ai * NB + r] = u;
           equ = fmax(equ, fabs(u));
           csum = u;
@@ -1038,7 +1042,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
         if (klo == 0 && khi == K1) {
           // whole time axis: rows K1.. of the table and of W are zero, columns beyond the live
           // ones only feed output rows/columns that are not stored: no masks
-          const double* tb = sTab + (size_t)kq * TS + colB;
+          const double* tb = sTab + (size_t)kq * TS + (colB ^ tab_swz(kq));   // k & 3 == kq
           const double* wa = sW + (size_t)kq * WSTR + rq;
           const int nks = (K1 + 3) >> 2;
           int ks = 0;
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           for (int q2 = 0; q2 < 2; ++q2) {
             const int k = 4 * (ks + q2) + kq;
             const bool kin = k >= klo && k < khi;
-            const double bv = (kin && colok) ? sTab[(size_t)k * TS + colB] : 0.0;
+            const double bv = (kin && colok) ? sTab[(size_t)k * TS + (colB ^ tab_swz(k))] : 0.0;
             const double* wk = sW + (size_t)k * WSTR;      // zero padded beyond NXI
             const double a0 = kin ? wk[rq] : 0.0;
             const double a1 = (kin && 8 + rq < NXI) ? wk[8 + rq] : 0.0;
@@ -1208,7 +1212,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
             double v = 0.0;
 #pragma unroll
             for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-            eqp = fmax(eqp, fabs(v - sBv[ai * NB + r]));
+            eqp = fmax(eqp, fabs(v - __ldg(gBv + ai * NB + r)));
           }
         }
 #pragma unroll
@@ -1280,7 +1284,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
             double v = 0.0;
 #pragma unroll
             for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-            const double u = sBv[ai * NB + r] - v;
+            const double u = __ldg(gBv + ai * NB + r) - v;
             sU[ai * NB + r] = u;
             equ = fmax(equ, fabs(u));
             csum += u;
