@@ -144,6 +144,12 @@ int64_t sfb_trajectory_metrics_work(int32_t n_members, int32_t n_d, int32_t n, i
 /* Dynamic shared memory one member needs (0 if the shape is unsupported). */
 int64_t sfb_smem_bytes(const sfb_plan* plan);
 
+/* Launch shape sfb_solve would use for n_members members with sfb_config.cluster = cluster and
+ * sfb_batch.flags = flags: the cluster size (auto-resolved when cluster <= 0), the dynamic shared
+ * memory per CTA and how many such CTAs one SM holds (capacity planning; no launch). */
+int sfb_launch_info(const sfb_plan* plan, int32_t n_members, int32_t cluster, int32_t flags,
+                    int32_t* cluster_out, int32_t* smem_out, int32_t* ctas_per_sm);
+
 const char* sfb_last_error(void);
 int32_t sfb_abi_version(void);
 

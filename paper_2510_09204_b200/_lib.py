@@ -16,7 +16,7 @@ SFB_OK, SFB_EINVAL, SFB_ESETUP, SFB_ECUDA, SFB_ENOMEM = 0, 1, 2, 3, 4
 MODE = {"projection": 0, "smoothness": 1}
 STATUS = {0: "max_iters", 1: "converged_primal", 2: "converged_fp"}
 EXPORTS = ("sfb_plan_create", "sfb_plan_destroy", "sfb_plan_cond", "sfb_solve",
-           "sfb_smem_bytes", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks",
+           "sfb_smem_bytes", "sfb_launch_info", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks",
            "sfb_trajectory_metrics", "sfb_trajectory_metrics_work")
 
 
@@ -79,6 +79,9 @@ def lib() -> ctypes.CDLL:
     L.sfb_plan_cond.restype = ctypes.c_double
     L.sfb_smem_bytes.argtypes = [vp]
     L.sfb_smem_bytes.restype = ctypes.c_int64
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    L.sfb_launch_info.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, i32p, i32p, i32p]
+    L.sfb_launch_info.restype = ctypes.c_int
     L.sfb_solve.argtypes = [vp, ctypes.POINTER(Batch), ctypes.POINTER(Config), ctypes.POINTER(Out), vp]
     L.sfb_solve.restype = ctypes.c_int
     L.sfb_kinematic_peaks.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

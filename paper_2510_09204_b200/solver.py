@@ -511,6 +511,15 @@ class DeviceBatch:
                              p(self.out_its), p(self.out_status), p(self.out_trace),
                              p(self.out_counters))
 
+    def launch_info(self) -> dict:
+        """Cluster size, shared memory per CTA and resident CTAs per SM of this batch's launch."""
+        c, sm, k = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        flags = _lib.BATCH_STATIC_OBSTACLES if self.obs_static else 0
+        rc = _lib.lib().sfb_launch_info(self.plan.handle, int(self.B), int(self.cluster), flags,
+                                        ctypes.byref(c), ctypes.byref(sm), ctypes.byref(k))
+        _lib.check(rc, "sfb_launch_info")
+        return {"cluster": c.value, "smem_bytes": sm.value, "ctas_per_sm": k.value}
+
     def launch(self, stream=None) -> None:
         """Enqueue the solve on `stream` (torch stream or None = current); no host sync."""
         import torch
