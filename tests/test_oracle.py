@@ -114,3 +114,22 @@ def test_metrics_oracle_matches_reference(name):
         got = trajectory_metrics(c, int(z["n_basis"]), int(z["num_steps"]), float(z["duration"]),
                                  obs, int(z["dense_factor"]))
         metrics_close(got, m)
+
+
+def test_kron_oracle_matches_live_reference_on_random_problems():
+    """Where the reference package is importable (this build container), a few random small
+    problems through its own generator / assemble / solve_batch against oracle/sf_kron.py
+    (oracle/fuzz_vs_reference.py runs the longer campaign)."""
+    import os
+    import subprocess
+    import sys
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        pytest.skip("reference package not present")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=ref_src, PYTHONDONTWRITEBYTECODE="1")
+    out = subprocess.run([sys.executable, os.path.join(root, "oracle", "fuzz_vs_reference.py"), "6", "11"],
+                         capture_output=True, text=True, env=env, cwd="/tmp", timeout=600)
+    if "No module named" in out.stderr:
+        pytest.skip("reference dependencies missing")
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
