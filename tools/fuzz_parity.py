@@ -17,7 +17,8 @@ from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble
 
 def one(rng, case):
     import dataclasses
-    n = int(rng.choice([1, 2, 3, 5, 8, 12, 16, 20, 31, 32, 33, 40]))
+    big = rng.random() < BIG_FRAC
+    n = int(rng.choice([48, 64, 80, 128])) if big else int(rng.choice([1, 2, 3, 5, 8, 12, 16, 20, 31, 32, 33, 40]))
     n_d = int(rng.choice([2, 2, 2, 3]))
     nxi = int(rng.integers(6, 13))
     K1 = int(rng.integers(max(nxi, 12), 110))
@@ -34,15 +35,27 @@ def one(rng, case):
     except Exception as e:   # generator cannot place this configuration
         return None, f"skip ({type(e).__name__})"
     sys_ = dataclasses.replace(assemble(scn, basis), d_max=d_max)
+    moving = m > 0 and rng.random() < MOVING_FRAC
+    if moving:   # linear obstacle tracks c + v t_k (per-step obstacle rows, no grid)
+        op = np.array(sys_.obs_pos, float)
+        v = 0.3 * rng.standard_normal(op.shape[:2])
+        t = np.linspace(0.0, 1.0, op.shape[2])
+        sys_ = dataclasses.replace(sys_, obs_pos=op[:, :, :1] + v[:, :, None] * t[None, None, :])
     xi = stack_xi(sample_naive_prior(scn, basis, S, seed=case))
     lam = 0.3 * np.random.default_rng(case).standard_normal(xi.shape)
     mm = lambda x: solver.to_member_major(x, n, nxi)
-    L = int(rng.integers(1, 60))
+    L = int(rng.integers(1, 12 if big else 60))
     fixed = rng.random() < 0.7
     cfg = solver.SolverConfig(rho=rho, max_iters=L, primal_tol=1e-3 if not fixed else 1e-3)
     cluster = int(rng.choice([0, 1, 2, 4]))
-    got = solver.solve_instances([sys_], mm(xi), mm(lam), mm(xi) if kind == "projection" else None,
-                                 kind=kind, cfg=cfg, fixed_iterations=fixed, cluster=cluster)
+    from paper_2510_09204_b200.errors import ShapeError
+    try:
+        got = solver.solve_instances([sys_], mm(xi), mm(lam), mm(xi) if kind == "projection" else None,
+                                     kind=kind, cfg=cfg, fixed_iterations=fixed, cluster=cluster)
+    except ShapeError as e:   # an explicit cluster size this layout cannot hold (auto falls back)
+        if cluster > 0 and "cluster" in str(e):
+            return None, f"skip (n={n} m={m} cluster={cluster}: {e})"
+        raise
     ref = sf_kron.solve_batch(sys_, xi, lam, kind=kind, target=xi if kind == "projection" else None,
                               rho=rho, max_iters=L, early_exit=not fixed)
     worst = 0.0
@@ -53,14 +66,21 @@ def one(rng, case):
             return False, f"iterations {got.iterations[b]} vs {ref['iterations'][b]}"
         tr = np.abs(got.trace[b][:, 0] - ref["trace"][b][:, 0]).max()
         worst = max(worst, rel, tr)
-    desc = (f"n={n} n_d={n_d} nxi={nxi} K1={K1} m={m} {kind} rho={rho} d_max={d_max:g} S={S} L={L} "
+    desc = (f"n={n} n_d={n_d} nxi={nxi} K1={K1} m={m}{' moving' if moving else ''} {kind} rho={rho} "
+            f"d_max={d_max:g} S={S} L={L} "
             f"{'fixed' if fixed else 'converge'} cluster={cluster}")
     return worst < 1e-8, f"{desc}: worst {worst:.2e}"
 
 
+BIG_FRAC, MOVING_FRAC = 0.0, 0.0
+
+
 def main():
+    global BIG_FRAC, MOVING_FRAC
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    BIG_FRAC = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0       # share of n in 48..128
+    MOVING_FRAC = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0    # share with moving obstacles
     rng = np.random.default_rng(seed)
     bad = 0
     for c in range(cases):
