@@ -52,6 +52,8 @@ def gather_fields(fields: dict, B_pad: int, dst: int = 0, trace_len: int | None 
     import torch
     import torch.distributed as dist
     flat = pack(fields, B_pad, trace_len)
+    if flat.is_cuda and dist.get_backend(group) == "gloo":   # gloo gathers host tensors only
+        flat = flat.cpu()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     bucket = [torch.empty_like(flat) for _ in range(world)] if rank == dst else None
