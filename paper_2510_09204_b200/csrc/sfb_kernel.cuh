@@ -230,10 +230,8 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 #endif
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
-// BIG2: the n > 32 kernel capped at 128 registers so that two CTAs share an SM (large
-// batches whose layout fits half the shared memory); BIG alone runs one CTA per SM
-template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
-__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
+template <int ND, int NXI, int NJ, bool BIG>
+__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
