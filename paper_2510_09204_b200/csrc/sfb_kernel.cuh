@@ -230,8 +230,10 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 #endif
 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
-template <int ND, int NXI, int NJ, bool BIG>
-__global__ void __launch_bounds__(NT, BIG ? 1 : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
+// BIG2 (n = 33..64, 2D): the n > 32 kernel capped at 128 registers, 8-warp CTAs, two per SM
+// (16 warps per SM; the uncapped build needs 230 registers and runs 4-warp CTAs)
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
+__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
