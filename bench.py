@@ -357,11 +357,15 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    n_res = 0
+    n_res, gaps = 0, []
     for res in solver.solve_stream(iter([step_in] * args.steps), cfg=cfg, fixed_iterations=True,
                                    trace=True):
         n_res += 1
+        gaps.append(time.perf_counter())
     t_e2e = time.perf_counter() - t0
+    if os.environ.get("BENCH_E2E_DEBUG"):
+        print("e2e yield gaps ms", [round((b - a) * 1e3, 1) for a, b in zip([t0] + gaps, gaps)],
+              file=sys.stderr)
     assert n_res == args.steps
     h2d = res.extra.get("h2d_bytes", 0)
     d2h = res.extra.get("d2h_bytes", 0)

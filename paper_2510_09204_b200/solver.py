@@ -342,6 +342,23 @@ def _pinned(n: int, which: str = "in"):
     return buf
 
 
+_STREAM_SLOTS: list = []     # idle solve_stream slots (pinned in/out arenas), grow-only pool
+
+
+def _checkout_slots(depth: int) -> list:
+    """Take `depth` slots from the pool (new ones are empty and pin their arenas on first
+    use). Pinning (cudaHostAlloc) costs 10-100+ ms and varies with host load, so a serving
+    loop must not pay it per stream; slots go back to the pool when the stream ends."""
+    got = []
+    while _STREAM_SLOTS and len(got) < depth:
+        got.append(_STREAM_SLOTS.pop())
+    while len(got) < depth:
+        got.append(dict(staging={}, out=None))
+    for s in got:
+        s["done"] = None
+    return got
+
+
 class DeviceBatch:
     """A batch of members (instance x sample) resident on one GPU.
 
@@ -684,23 +701,25 @@ def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projectio
 
 
 def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = None,
-                 fixed_iterations: bool = False, trace: bool = True, cluster: int = 0):
+                 fixed_iterations: bool = False, trace: bool = True, cluster: int = 0, depth: int = 3):
     """Pipelined solve_instances over a sequence of batches (the serving loop): yields one
     BatchResult per step, in order. `steps` yields (systems, xi0, lam0, target,
     member_instance) tuples of host (or CUDA) arrays.
 
     Every step still packs its inputs into a pinned arena, copies them to the device and
     reads its whole output arena back; those copies run on a copy stream and the host
-    packing runs ahead, so they overlap the neighbouring steps' kernels (double-buffered
-    pinned and device arenas; step k+2 reuses step k's buffers only after step k's copies
-    completed)."""
+    packing runs ahead, so they overlap the neighbouring steps' kernels. `depth` steps are in
+    flight (pinned and device arenas per slot; step k + depth reuses step k's buffers only after
+    step k's copies completed): the host may fall behind by depth - 1 kernels (scheduling
+    jitter on a busy host) before the GPU idles."""
+    depth = max(2, int(depth))
     import torch
     cfg = cfg or SolverConfig()
     dev = torch.device("cuda", torch.cuda.current_device())
     compute = torch.cuda.current_stream(dev)
     copy_in, copy_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)   # H2D of step k+1 must
     # not queue behind the D2H of step k (which waits for kernel k)
-    slots = [dict(staging=None, out=None, done=None) for _ in range(2)]
+    slots = _checkout_slots(depth)
     pending = []    # (batch, slot, d2h event, t0)
 
     def finish(item):
@@ -725,13 +744,24 @@ def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = Non
                            extra={"h2d_bytes": batch.h2d_bytes,
                                   "d2h_bytes": int(batch._out_arena.numel()) * 8})
 
+    try:
+        yield from _stream_loop(steps, slots, pending, finish, depth, compute, copy_in, copy_out,
+                                kind, cfg, fixed_iterations, trace, cluster)
+    finally:
+        for s in slots:                           # copies still in flight finish before reuse
+            if s["done"] is not None:
+                s["done"].synchronize()
+        _STREAM_SLOTS.extend(slots)
+
+
+def _stream_loop(steps, slots, pending, finish, depth, compute, copy_in, copy_out,
+                 kind, cfg, fixed_iterations, trace, cluster):
+    import torch
     for k, (systems, xi0, lam0, target, mi) in enumerate(steps):
         t0 = time.perf_counter()
-        slot = slots[k & 1]
+        slot = slots[k % depth]
         if slot["done"] is not None:
-            slot["done"].synchronize()            # this slot's copies of step k-2 completed
-        if slot["staging"] is None:
-            slot["staging"] = {}
+            slot["done"].synchronize()            # this slot's copies of step k - depth completed
         batch = DeviceBatch(systems, xi0, lam0, target, kind=kind, cfg=cfg, member_instance=mi,
                             early_exit=not fixed_iterations, trace=trace, cluster=cluster,
                             staging=slot["staging"], copy_stream=copy_in)
@@ -753,7 +783,7 @@ def solve_stream(steps, kind: str = "projection", cfg: SolverConfig | None = Non
         ev_out.record(copy_out)
         slot["done"] = ev_out
         pending.append((batch, dict(out=slot["out"][:nout]), ev_out, t0))
-        if len(pending) > 1:
+        if len(pending) >= depth:
             yield finish(pending.pop(0))
     while pending:
         yield finish(pending.pop(0))
