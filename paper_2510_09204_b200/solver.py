@@ -159,20 +159,16 @@ def _dense_kkt_cond(sys, kind: str, rho: float) -> float:
     return float(np.linalg.cond(M))
 
 
-_A_OK: dict = {}
-
-
 def _kron_checked(A: np.ndarray, n: int, E: np.ndarray) -> bool:
-    """A == I_n (x) E, memoised on the identity and contents fingerprint of A."""
-    key = (id(A), A.__array_interface__["data"][0], A.shape, float(A.sum()), float(np.abs(A).sum()))
-    hit = _A_OK.get(key)
-    if hit is not None:
-        return hit
-    ok = bool(np.array_equal(A, np.kron(np.eye(n), E)))
-    if len(_A_OK) > 4096:
-        _A_OK.clear()
-    _A_OK[key] = ok
-    return ok
+    """A == I_n (x) E: every diagonal block equals E and nothing outside the diagonal blocks
+    is non-zero (a view and two reductions; no n x n Kronecker product is formed)."""
+    nb, nx = E.shape
+    if A.shape != (n * nb, n * nx):
+        return False
+    r = np.arange(n)
+    diag = A.reshape(n, nb, n, nx)[r, :, r, :]           # (n, nb, nx)
+    return bool(np.array_equal(diag, np.broadcast_to(E, diag.shape))
+                and np.count_nonzero(A) == np.count_nonzero(diag))
 
 
 _SD: dict = {}

@@ -3,7 +3,7 @@ robots x batch sweep (C5: 8-128 robots, batch 1-1024 instances, 20 obstacles,
 box half-width max(1, 2 sqrt(n/32)), T=100, L=500). Device-timed
 (CUDA events, inputs resident), one GPU. Writes profiles/r02_sweep.json.
 
-    python tools/sweep.py [--quick]
+    python tools/sweep.py [--quick] [--out=<file name under profiles/>]
 """
 import json
 import math
@@ -56,6 +56,7 @@ def time_solve(systems, xi, mi, L, reps=3):
 
 def main():
     quick = "--quick" in sys.argv
+    out = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")), "r02_sweep.json")
     L = 500
     rows = []
     named = [("C1", 4, 0, 1.0, 1, 1), ("C2", 16, 10, 1.0, 32, 1), ("C3", 32, 20, 2.0, 64, 8),
@@ -72,15 +73,13 @@ def main():
     for n in robots:
         h = max(1.0, 2.0 * math.sqrt(n / 32))
         for inst in batches:
-            if n == 128 and inst > 256:
-                continue
             systems, xi, mi = workload(n, 20, h, inst, 1, 5000 + n)
             t, smem = time_solve(systems, xi, mi, L, reps=2)
             rows.append(dict(config="C5", robots=n, obstacles=20, instances=inst, samples=1,
                              members=inst, L=L, seconds=t, instances_per_s=inst / t,
                              member_iters_per_s=inst * (L + 1) / t, smem_bytes=smem))
             print(json.dumps(rows[-1]), flush=True)
-    with open(os.path.join(ROOT, "profiles", "r02_sweep.json"), "w") as fh:
+    with open(os.path.join(ROOT, "profiles", out), "w") as fh:
         json.dump({"gpu": torch.cuda.get_device_name(0), "rows": rows,
                    "note": "device-timed solve (CUDA events), inputs resident; C5 uses 20 obstacles, "
                            "box half-width max(1, 2 sqrt(n/32)), 1 sample, naive-prior warm start"},
