@@ -338,6 +338,8 @@ def _pinned(n: int, which: str = "in"):
     return buf
 
 
+SMALL_D2H_BYTES = 1 << 20   # output arenas up to this size are read back in one copy
+
 _STREAM_SLOTS: list = []     # idle solve_stream slots (pinned in/out arenas), grow-only pool
 
 
@@ -546,8 +548,12 @@ class DeviceBatch:
         only up to the longest member's iterations). Member-major arrays."""
         import torch
         B, n_d, n, n_xi = self.out_xi.shape
-        head = _pinned(self._out_prefix, "out")[: self._out_prefix]
-        head.copy_(self._out_arena[: self._out_prefix])
+        # a small arena (the latency case) crosses in one copy with the whole trace; a large
+        # one copies the head first, then the trace only up to the longest member's iterations
+        one_copy = self.out_trace is not None and self._out_arena.numel() * 8 <= SMALL_D2H_BYTES
+        nh = self._out_arena.numel() if one_copy else self._out_prefix
+        head = _pinned(nh, "out")[:nh]
+        head.copy_(self._out_arena[:nh])
         head = head.numpy()
         o = self._oofs
         get = lambda k: head[o[k][0]: o[k][0] + o[k][1]]
@@ -561,10 +567,13 @@ class DeviceBatch:
         d2h = head.nbytes
         if self.out_trace is not None:
             T = int(its.max()) + 1 if its.size else 0
-            tr = _pinned(B * T * 2, "trace")[: B * T * 2].view(B, T, 2)
-            tr.copy_(self.out_trace[:, :T])
-            tr = tr.numpy().copy()
-            d2h += tr.nbytes
+            if one_copy:
+                tr = get("trace").reshape(B, -1, 2)[:, :T].copy()
+            else:
+                tr = _pinned(B * T * 2, "trace")[: B * T * 2].view(B, T, 2)
+                tr.copy_(self.out_trace[:, :T])
+                tr = tr.numpy().copy()
+                d2h += tr.nbytes
             out["trace"] = [tr[b, : its[b] + 1] for b in range(B)]
         if self.out_counters is not None:
             out["counters"] = self.out_counters.cpu().numpy()
