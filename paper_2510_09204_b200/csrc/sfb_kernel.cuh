@@ -981,27 +981,48 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     if (TBL) {
       const int ncu = ND * NB, ntask = ts_hi - ts_lo, R = ntask % nw, Lw = nw - R;
       int t0 = warp, dt = nw;                       // spread over every warp ...
-      if (R != 0 && Lw >= 4) {                      // ... or over the lighter ones
-        t0 = warp >= R ? warp - R : ncu;
+      if (R != 0 && (Lw >= 4 || ntask < nw)) {      // ... or over the lighter ones (in cluster
+        t0 = warp >= R ? warp - R : ncu;            // mode, the warps that had no task at all)
         dt = Lw;
       }
-      for (int t = t0; t < ncu; t += dt) {
-        const int a = (t >= NB) + (ND == 3 && t >= 2 * NB), r = t - a * NB;
-        double csum = 0.0;
-        if (lane < n) {
-          const int ai = a * n + lane;
-          const double* x = sXi + ai * NXP;
-          double v = 0.0;
+      // UCB columns per pass with independent chains (the per-column arithmetic and the xor
+      // tree are unchanged: same bits)
+      constexpr int UCB = 4;
+      for (int tb = t0; tb < ncu; tb += UCB * dt) {
+        double csum[UCB];
 #pragma unroll
-          for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
-          const double u = __ldg(gBv + ai * NB + r) - v;
-          sU[ai * NB + r] = u;
-          equ = fmax(equ, fabs(u));
-          csum = u;
+        for (int q = 0; q < UCB; ++q) {           // loads and arithmetic first ...
+          const int t = tb + q * dt;
+          csum[q] = 0.0;
+          if (t < ncu && lane < n) {
+            const int a = (t >= NB) + (ND == 3 && t >= 2 * NB), r = t - a * NB;
+            const int ai = a * n + lane;
+            const double* x = sXi + ai * NXP;
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < NXI; ++c) v = fma(sE[r * NXI + c], x[c], v);
+            const double u = __ldg(gBv + ai * NB + r) - v;
+            equ = fmax(equ, fabs(u));
+            csum[q] = u;
+          }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) csum += __shfl_xor_sync(FULL, csum, off);
-        if (lane == 0) sSU[t] = csum;
+        for (int q = 0; q < UCB; ++q) {           // ... then the stores
+          const int t = tb + q * dt;
+          if (t < ncu && lane < n) {
+            const int a = (t >= NB) + (ND == 3 && t >= 2 * NB), r = t - a * NB;
+            sU[(a * n + lane) * NB + r] = csum[q];
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < UCB; ++q) csum[q] += __shfl_xor_sync(FULL, csum[q], off);
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < UCB; ++q)
+            if (tb + q * dt < ncu) sSU[tb + q * dt] = csum[q];
+        }
       }
     }
     if (!BIG && RA > 0) {
@@ -1246,9 +1267,17 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     // residual of the xi committed at it-1, solver.py:336-337). Sums use a fixed xor tree.
     double fpp = 0.0;
     const int ncolD = ND * NXI, ncol = ncolD + (TBL ? 0 : ND * NB);
-    for (int col = warp; col < ncol; col += nw) {
+    // UC1 columns per pass (warp w: columns w, w + nw, ... in that order), independent chains;
+    // the per-column arithmetic, the fpp order and the xor tree are unchanged
+    constexpr int UC1 = 3;
+    for (int cb = warp; cb < ncol; cb += UC1 * nw) {
+     double csumv[UC1];
+#pragma unroll
+     for (int q = 0; q < UC1; ++q) {
+      const int col = cb + q * nw;
       double csum = 0.0;
-      if (col < ncolD) {
+      if (col >= ncol) {
+      } else if (col < ncolD) {
         const int a = col / NXI, c = col - a * NXI;
         for (int i0 = 0; i0 < (BIG ? n : 1); i0 += 32) {   // n <= 32: one pass
           const int ii = i0 + lane;
@@ -1291,12 +1320,20 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           }
         }
       }
+      csumv[q] = csum;
+     }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) csum += __shfl_xor_sync(FULL, csum, off);
-      if (lane == 0) {
-        if (col < ncolD) sSD[col] = csum;
-        else sSU[col - ncolD] = csum;
-      }
+     for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+       for (int q = 0; q < UC1; ++q) csumv[q] += __shfl_xor_sync(FULL, csumv[q], off);
+     if (lane == 0) {
+#pragma unroll
+       for (int q = 0; q < UC1; ++q) {
+         const int col = cb + q * nw;
+         if (col < ncolD) sSD[col] = csumv[q];
+         else if (col < ncol) sSU[col - ncolD] = csumv[q];
+       }
+     }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) equ = fmax(equ, __shfl_xor_sync(FULL, equ, off));
