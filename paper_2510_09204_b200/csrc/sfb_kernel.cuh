@@ -53,6 +53,7 @@ struct Layout {       // byte offsets into dynamic shared memory
   int grid;           // static-obstacle candidate grid [GRID][GRID] u32 (compact mode)
   int kc;             // per-member constants read at their (rare) use sites: KC_* below
   int ub;             // TBL: boundary rows u [ND*n][NB] + their robot sums [ND][NB]
+  int pb;             // TBL: [Pxx | Pxb]^T as DMMA B fragments [k-step][8-column tile][lane]
   int xg;             // cluster exchange buffers [2][nv + 2] (set at launch when csize > 1)
   int uni_bytes, total;
   int slots;          // G partial slots that fit in the union region per round
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   double* sQ = reinterpret_cast<double*>(smem + P.L.q);      // [NXI][NXI]
   double* sPxx = reinterpret_cast<double*>(smem + P.L.pxx);
   double* sPxb = reinterpret_cast<double*>(smem + P.L.pxb);
+  double* sPB = reinterpret_cast<double*>(smem + P.L.pb);
   double* sDxx = reinterpret_cast<double*>(smem + P.L.dxx);
   double* sDxb = reinterpret_cast<double*>(smem + P.L.dxb);
   double* sG = reinterpret_cast<double*>(smem + P.L.g);      // [ND*n][NXI]
@@ -324,6 +326,14 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   for (int idx = tid; idx < NXI * NB; idx += nt) {
     sPxb[idx] = P.consts[co.Pxb + idx];
     sDxb[idx] = P.consts[co.Dxb + idx];
+  }
+  if (TBL) {   // E2's B operand, fragment-ordered and zero padded: one unconditional LDS.64 each
+    const int KT = NXI + NB, nks = (KT + 3) >> 2;
+    for (int idx = tid; idx < nks * 64; idx += nt) {
+      const int ks = idx >> 6, c = ((idx >> 5) & 1) * 8 + ((idx & 31) >> 2), k = 4 * ks + (idx & 3);
+      sPB[idx] = (c < NXI && k < KT) ? ((k < NXI) ? P.consts[co.Pxx + c * NXI + k]
+                                                  : P.consts[co.Pxb + c * NB + (k - NXI)]) : 0.0;
+    }
   }
   {
     const double* x0 = P.xi0 + (size_t)b * nv;
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
 
 #ifdef SFB_PHASE_TIMING
-  long long t_ph[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t_last = clock64(), t_sub = t_last;
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
@@ -1340,6 +1350,9 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     if (lane == 0) sRed[warp * 4 + 2] = equ;
     __syncthreads();
     SFB_TMARK(4);
+#ifdef SFB_PHASE_TIMING
+    if (tid == 0) t_sub = clock64();
+#endif
     if (it > 0) {
       #pragma unroll
         for (int w = 0; w < NW; ++w)
@@ -1370,6 +1383,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
         }
         mv[h] = m0 + m1;
       }
+      SFB_TSUB(14);
       for (int tl = warp; tl < nmt; tl += nw) {
         const int row = tl * 8 + rq;
         const bool rowok = row < nrow;
@@ -1389,16 +1403,26 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
             }
             acc[nt2][j] = (rowok && c < NXI) ? sXi[row * NXP + c] + mval : 0.0;
           }
-        for (int ks = 0; ks < (KT + 3) >> 2; ++ks) {
-          const int k = 4 * ks + kq;
-          double av = 0.0;
-          if (rowok) av = (k < NXI) ? sD[row * NXI + k] : ((k < KT) ? sU[row * NB + (k - NXI)] : 0.0);
+        // all fragments first (no branches between the loads), then the DMMA chain; the
+        // operands and the k order are those of the per-step form (same bits)
+        constexpr int KSM = (NXI + NBM + 3) / 4;
+        const int nks = (KT + 3) >> 2;
+        double av[KSM], bv[KSM][2];
 #pragma unroll
-          for (int nt2 = 0; nt2 < 2; ++nt2) {
-            const int c = nt2 * 8 + rq;
-            const double bv = (c < NXI && k < KT) ? ((k < NXI) ? sPxx[c * NXI + k] : sPxb[c * NB + (k - NXI)]) : 0.0;
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                         : "+d"(acc[nt2][0]), "+d"(acc[nt2][1]) : "d"(av), "d"(bv));
+        for (int ks = 0; ks < KSM; ++ks) {
+          const int k = 4 * ks + kq;
+          const double* ap = (k < NXI) ? sD + row * NXI + k : sU + row * NB + (k - NXI);
+          av[ks] = (rowok && k < KT) ? *ap : 0.0;
+          bv[ks][0] = ks < nks ? sPB[(ks * 2) * 32 + lane] : 0.0;
+          bv[ks][1] = ks < nks ? sPB[(ks * 2 + 1) * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < KSM; ++ks) {
+          if (ks < nks) {
+#pragma unroll
+            for (int nt2 = 0; nt2 < 2; ++nt2)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(acc[nt2][0]), "+d"(acc[nt2][1]) : "d"(av[ks]), "d"(bv[ks][nt2]));
           }
         }
 #pragma unroll
@@ -1415,6 +1439,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
             }
           }
       }
+      SFB_TSUB(15);
     } else
     for (int col = warp; col < ncolD; col += nw) {
       const int a = col / NXI, c = col - a * NXI;
@@ -1457,7 +1482,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   }
 #ifdef SFB_PHASE_TIMING  // @stage epilogue
   if (tid == 0 && P.counters) {
-    for (int q = 0; q < 14; ++q) P.counters[(size_t)b * 20 + 4 + q] = (unsigned long long)t_ph[q];
+    for (int q = 0; q < 16; ++q) P.counters[(size_t)b * 20 + 4 + q] = (unsigned long long)t_ph[q];
   }
 #endif
 

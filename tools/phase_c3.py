@@ -23,9 +23,9 @@ batch.launch(); torch.cuda.synchronize()
 c = batch.out_counters.cpu().numpy().astype(float)
 names = ["tasks", "bar_after_tasks", "G_reduce", "decision", "K1+bar", "K2+K3+bar"]
 sub_names = ["  positions", "  robot screen", "  robot exact", "  obstacles", "  box+contract",
-             "  cluster.sync", "  dsmem reads", "  post-read bar"]
+             "  cluster.sync", "  dsmem reads", "  post-read bar", "  E2 mean", "  E2 dmma+store"]
 per = c[:, 4:10].mean(axis=0) / (L + 1)
-sub = c[:, 10:18].mean(axis=0) / (L + 1)
+sub = c[:, 10:20].mean(axis=0) / (L + 1)
 tot = per.sum()
 for nm, v in zip(names, per):
     print(f"{nm:18s} {v:9.0f} cycles/iter ({v / tot * 100:5.1f}%)")
