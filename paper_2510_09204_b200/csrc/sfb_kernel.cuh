@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
 
 #ifdef SFB_PHASE_TIMING
-  long long t_ph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_ph[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t_last = clock64(), t_sub = t_last;
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
@@ -1053,6 +1053,9 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     SFB_TMARK(0);
     __syncthreads();   // all positions consumed: the union region is free
     SFB_TMARK(1);
+#ifdef SFB_PHASE_TIMING
+    if (tid == 0) t_sub = clock64();
+#endif
 
     if (TBL) {
       // G^T (c x col) = W^T (c x k) . g (k x col) on the FP64 tensor cores (DMMA m8n8k4): warp
@@ -1122,6 +1125,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
           }
         }
       }
+      SFB_TSUB(16);
       __syncthreads();
     } else if (!BIG) {
       // G = sum over warps, then over the k-group sub-lanes, of the per-lane partials (fixed order)
@@ -1271,6 +1275,9 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     }
 
     SFB_TMARK(3);
+#ifdef SFB_PHASE_TIMING
+    if (tid == 0) t_sub = clock64();
+#endif
     // -------------------------------------------- E: multiplier update and KKT step  // @stage E1_kkt
     // E1: one warp per column, lanes = robots. Columns (a, c): lambda+, Delta and the robot
     // sum of Delta; columns (a, r): u = b - E xi, its robot sum, and max|u| (the boundary
@@ -1345,6 +1352,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
        }
      }
     }
+    SFB_TSUB(17);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) equ = fmax(equ, __shfl_xor_sync(FULL, equ, off));
     if (lane == 0) sRed[warp * 4 + 2] = equ;
@@ -1482,7 +1490,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   }
 #ifdef SFB_PHASE_TIMING  // @stage epilogue
   if (tid == 0 && P.counters) {
-    for (int q = 0; q < 16; ++q) P.counters[(size_t)b * 20 + 4 + q] = (unsigned long long)t_ph[q];
+    for (int q = 0; q < 18; ++q) P.counters[(size_t)b * 24 + 4 + q] = (unsigned long long)t_ph[q];
   }
 #endif
 
@@ -1496,7 +1504,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     }
     if (lane == 0) {
 #ifdef SFB_PHASE_TIMING
-      unsigned long long* cb = P.counters + (size_t)b * 20;
+      unsigned long long* cb = P.counters + (size_t)b * 24;
 #else
       unsigned long long* cb = P.counters + (size_t)b * 4;
 #endif

@@ -16,16 +16,17 @@ systems, xi, mi = systems[:n_inst], xi[sel], mi[sel]
 batch = solver.DeviceBatch(systems, xi, None, xi, cfg=solver.SolverConfig(max_iters=L),
                            member_instance=mi, early_exit=False, trace=False, counters=True,
                            cluster=cluster)
-batch.out_counters = torch.zeros((batch.B, 20), dtype=torch.int64, device=batch.device)
+batch.out_counters = torch.zeros((batch.B, 24), dtype=torch.int64, device=batch.device)
 batch._build_structs()
 batch.launch(); torch.cuda.synchronize()
 batch.launch(); torch.cuda.synchronize()
 c = batch.out_counters.cpu().numpy().astype(float)
 names = ["tasks", "bar_after_tasks", "G_reduce", "decision", "K1+bar", "K2+K3+bar"]
 sub_names = ["  positions", "  robot screen", "  robot exact", "  obstacles", "  box+contract",
-             "  cluster.sync", "  dsmem reads", "  post-read bar", "  E2 mean", "  E2 dmma+store"]
+             "  cluster.sync", "  dsmem reads", "  post-read bar", "  E2 mean", "  E2 dmma+store",
+             "  G contraction (own tile)", "  E1 columns (own)"]
 per = c[:, 4:10].mean(axis=0) / (L + 1)
-sub = c[:, 10:20].mean(axis=0) / (L + 1)
+sub = c[:, 10:22].mean(axis=0) / (L + 1)
 tot = per.sum()
 for nm, v in zip(names, per):
     print(f"{nm:18s} {v:9.0f} cycles/iter ({v / tot * 100:5.1f}%)")
