@@ -113,3 +113,23 @@ def test_bench_roofline_model_numbers():
     o32, o64 = bench.algorithmic_ops(32, 20, 100, 11, 2, 6, 0, 1)
     # C3 screened FP32 0.874 M at A = 0, FP64 ~0.184 M
     assert abs(o32 - 873_600) < 1 and abs(o64 - 183_852) < 1
+
+
+def test_kron_structure_check_matches_dense_kronecker():
+    """solver._kron_checked (diagonal blocks + non-zero count) agrees with the dense
+    A == kron(I_n, E) comparison it replaced, on exact, perturbed, NaN and misplaced entries."""
+    rng = np.random.default_rng(5)
+    for n, nb, nx in [(1, 6, 11), (3, 2, 5), (8, 6, 11), (32, 6, 11)]:
+        E = rng.standard_normal((nb, nx))
+        E[rng.random(E.shape) < 0.3] = 0.0
+        A = np.kron(np.eye(n), E)
+        assert solver._kron_checked(A, n, E)
+        cases = []
+        B = A.copy(); B[0, -1] = 1e-300; cases.append(B)                # off-diagonal block
+        B = A.copy(); B[-1, 0] = -2.0; cases.append(B)
+        B = A.copy(); B[nb - 1, nx - 1] += 1e-12; cases.append(B)       # diagonal block differs
+        B = A.copy(); B[0, 0] = np.nan; cases.append(B)
+        for B in cases:
+            dense = bool(np.array_equal(B, np.kron(np.eye(n), E)))
+            assert solver._kron_checked(B, n, E) == dense
+        assert not solver._kron_checked(A[:, :-1], n, E)                 # wrong shape
