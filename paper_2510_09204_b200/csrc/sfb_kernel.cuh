@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   long long t_last = clock64(), t_sub = t_last;
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-  double eq_max = 0.0;
+  double eq_max = 0.0, eql = 0.0;
   // per-thread counts fit 32 bits (rows of one lane over one solve); summed in 64 bits at the end
   unsigned c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     if (conv_p || conv_f || it == P.max_iters) {
       // the xi committed at it-1 has not had its boundary residual measured yet
       if (it > 0) {
-        double eqp = 0.0;
+        double eqp = eql;   // this lane's running max over the earlier committed steps
         for (int ai = tid; ai < nrows; ai += nt) {
           const double* x = sXi + ai * NXP;
           for (int r = 0; r < NB; ++r) {
@@ -1353,19 +1353,14 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
      }
     }
     SFB_TSUB(17);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) equ = fmax(equ, __shfl_xor_sync(FULL, equ, off));
-    if (lane == 0) sRed[warp * 4 + 2] = equ;
+    // boundary residual max over committed steps: a per-lane running max, reduced over the CTA
+    // once at exit (max is order-free: the same value as a per-iteration reduction)
+    if (it > 0) eql = fmax(eql, equ);
     __syncthreads();
     SFB_TMARK(4);
 #ifdef SFB_PHASE_TIMING
     if (tid == 0) t_sub = clock64();
 #endif
-    if (it > 0) {
-      #pragma unroll
-        for (int w = 0; w < NW; ++w)
-          if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
-    }
     // E2: xi+ = xi + Pxx Delta_i + Pxb u_i + (Dxx sum Delta + Dxb sum u)  // @stage E2_kkt
 #ifndef SFB_E2_SIMT
 #define SFB_E2_SIMT 0   // experiments: 1 runs the SIMT xi update also on the TBL path
