@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
 #endif
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   double eq_max = 0.0, eql = 0.0;
+  double fpp = 0.0;   // per-lane ||dlambda||^2 + ||dxi||^2 partial of the last KKT step
   // per-thread counts fit 32 bits (rows of one lane over one solve); summed in 64 bits at the end
   unsigned c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
@@ -1041,14 +1042,18 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
 #pragma unroll
         for (int c = 0; c < NXI; ++c) gl[(c * ND + a) * 32] = Gp[a][c];
     }
+    // fpp: the previous iteration's per-lane fixed-point partial, reduced here next to s1, s2
+    // (its xor tree used to end the KKT step on the serial path; same tree, same value)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       s1 += __shfl_xor_sync(FULL, s1, off);
       s2 += __shfl_xor_sync(FULL, s2, off);
+      fpp += __shfl_xor_sync(FULL, fpp, off);
     }
     if (lane == 0) {
       sRed[warp * 4 + 0] = s1;
       sRed[warp * 4 + 1] = s2;
+      sRed[warp * 4 + 3] = fpp;
     }
     SFB_TMARK(0);
     __syncthreads();   // all positions consumed: the union region is free
@@ -1282,7 +1287,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     // E1: one warp per column, lanes = robots. Columns (a, c): lambda+, Delta and the robot
     // sum of Delta; columns (a, r): u = b - E xi, its robot sum, and max|u| (the boundary
     // residual of the xi committed at it-1, solver.py:336-337). Sums use a fixed xor tree.
-    double fpp = 0.0;
+    fpp = 0.0;
     const int ncolD = ND * NXI, ncol = ncolD + (TBL ? 0 : ND * NB);
     // UC1 columns per pass (warp w: columns w, w + nw, ... in that order), independent chains;
     // the per-column arithmetic, the fpp order and the xor tree are unchanged
@@ -1477,9 +1482,6 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
         }
       }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) fpp += __shfl_xor_sync(FULL, fpp, off);
-    if (lane == 0) sRed[warp * 4 + 3] = fpp;
     __syncthreads();
     SFB_TMARK(5);
   }
