@@ -141,6 +141,23 @@ int sfb_trajectory_metrics(const double* coeffs, int32_t n_members, int32_t n_d,
 int64_t sfb_trajectory_metrics_work(int32_t n_members, int32_t n_d, int32_t n, int32_t n_basis,
                                     int32_t k_dense, int32_t n_obs);
 
+/* Analysis intermediates of one map evaluation's INPUT coefficients, as the reference's
+ * fixed_point_step returns them (solver.py:246-256 -> _analyze, solver.py:158-169): the
+ * spherical variables of every separation row (extract_spherical, constraints.py:195-213,
+ * the reference's atan2 / sin / cos closed forms) and the workspace slack
+ * s = max(0, h - G xi) (solver.py:166-167). coeffs [B][n_d][n][n_basis]; member b reads
+ * instance member_instance[b] of pair_axes [I][3], obs_axes [I][n_obs][3],
+ * obs_pos [I][n_d][n_obs][num_steps] and box [I][2][n_d]; W [num_steps][n_basis].
+ * Outputs in the reference's layouts (batch axis last): alpha, beta, d [n_pairs][num_steps][B]
+ * (pairs i < j, lexicographic), alpha_o, beta_o, d_o [n][n_obs][num_steps][B],
+ * s [n_d][2 n num_steps][B]. All pointers on the device; stream-ordered. */
+int sfb_analysis_vars(const double* coeffs, int32_t n_members, const int32_t* member_instance,
+                      int32_t n_d, int32_t n, int32_t n_basis, int32_t num_steps, int32_t n_obs,
+                      const double* W, const double* pair_axes, const double* obs_axes,
+                      const double* obs_pos, const double* box, double d_max, double* alpha,
+                      double* beta, double* d, double* alpha_o, double* beta_o, double* d_o,
+                      double* s, void* stream);
+
 /* Dynamic shared memory one member needs (0 if the shape is unsupported). */
 int64_t sfb_smem_bytes(const sfb_plan* plan);
 

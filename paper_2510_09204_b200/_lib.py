@@ -17,7 +17,7 @@ MODE = {"projection": 0, "smoothness": 1}
 STATUS = {0: "max_iters", 1: "converged_primal", 2: "converged_fp"}
 EXPORTS = ("sfb_plan_create", "sfb_plan_destroy", "sfb_plan_cond", "sfb_solve",
            "sfb_smem_bytes", "sfb_launch_info", "sfb_last_error", "sfb_abi_version", "sfb_kinematic_peaks",
-           "sfb_trajectory_metrics", "sfb_trajectory_metrics_work")
+           "sfb_trajectory_metrics", "sfb_trajectory_metrics_work", "sfb_analysis_vars")
 
 
 class Dims(ctypes.Structure):
@@ -93,6 +93,9 @@ def lib() -> ctypes.CDLL:
     L.sfb_trajectory_metrics.restype = ctypes.c_int
     L.sfb_trajectory_metrics_work.argtypes = [i32, i32, i32, i32, i32, i32]
     L.sfb_trajectory_metrics_work.restype = ctypes.c_int64
+    L.sfb_analysis_vars.argtypes = [vp, i32, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp,
+                                    ctypes.c_double, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.sfb_analysis_vars.restype = ctypes.c_int
     L.sfb_last_error.argtypes = []
     L.sfb_last_error.restype = ctypes.c_char_p
     L.sfb_abi_version.argtypes = []

@@ -10,7 +10,7 @@ producing the same numbers the reference would:
 * `generate` restates the random-box / antipodal-circle generators of
   `pkg/src/swarmplan/scenario.py:116-188` with the same RNG call sequence, so a
   seed yields the reference's scenario bit for bit (checked in
-  `tests/test_problem.py` against the reference in the dev container).
+  `tests/test_host.py:82-108` against the reference in the dev container).
 * `assemble` restates the parts of `pkg/src/swarmplan/constraints.py:95-156`
   the B200 solver needs: the boundary matrix A = I_n (x) E and b, the workspace
   bounds h, the obstacle trajectories and the inflated contact axes. The dense

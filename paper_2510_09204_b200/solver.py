@@ -77,6 +77,19 @@ class SolverState:
 
 
 @dataclass
+class SphericalVars:
+    """constraints.py:70-81: spherical reformulation variables, trailing batch axis.
+    alpha/beta/d: (n_pairs, K+1, B); alpha_o/beta_o/d_o: (n, n_obs, K+1, B)."""
+
+    alpha: np.ndarray
+    beta: np.ndarray
+    d: np.ndarray
+    alpha_o: np.ndarray
+    beta_o: np.ndarray
+    d_o: np.ndarray
+
+
+@dataclass
 class SolverResult:
     """solver.py:108-129."""
 
@@ -195,6 +208,56 @@ def system_data(sys, kind: str = "projection", rho: float = 1.0) -> SystemData:
     return sd
 
 
+def _check_selection_structure(sys, W: np.ndarray) -> None:
+    """The plan's KKT blocks assume the F, G and pair list `assemble` builds
+    (constraints.py:122-139): every pair i < j in lexicographic order, then every
+    (robot, obstacle) row, F = [D (x) W; I (x) (1_m (x) W)] and G = [I (x) W; -I (x) W].
+    A reference system carrying its dense F / G is checked structurally (shapes, index
+    lists, a fixed sample of rows) so a different selection is refused instead of being
+    solved with the wrong KKT matrix."""
+    d = sys.dims
+    n, K1, n_xi, m = d.n, d.num_steps, d.n_basis, d.n_obs
+    pairs = getattr(sys, "pair_index", None)
+    if pairs is not None and [tuple(p) for p in pairs] != [(i, j) for i in range(n) for j in range(i + 1, n)]:
+        raise UsageError("pair_index is not the full lexicographic pair list: unsupported constraint system")
+    obs_index = getattr(sys, "obs_index", None)
+    if obs_index is not None and [tuple(p) for p in obs_index] != [(i, o) for i in range(n) for o in range(m)]:
+        raise UsageError("obs_index is not the full (robot, obstacle) list: unsupported constraint system")
+    P = n * (n - 1) // 2
+    F = getattr(sys, "F", None)
+    if F is not None:
+        F = np.asarray(F)
+        if F.shape != ((P + n * m) * K1, n * n_xi):
+            raise UsageError(f"F has shape {F.shape}, expected {((P + n * m) * K1, n * n_xi)}")
+        rows = sorted({0, K1 - 1, P * K1 - 1, P * K1, F.shape[0] - 1, (P // 2) * K1 + K1 // 2}
+                      & set(range(F.shape[0])))
+        for r in rows:
+            want = np.zeros(n * n_xi)
+            k = r % K1
+            if r < P * K1:
+                i, j = [(i, j) for i in range(n) for j in range(i + 1, n)][r // K1]
+                want[i * n_xi:(i + 1) * n_xi] = W[k]
+                want[j * n_xi:(j + 1) * n_xi] = -W[k]
+            else:
+                i = (r - P * K1) // (m * K1)
+                want[i * n_xi:(i + 1) * n_xi] = W[k]
+            if not np.array_equal(F[r], want):
+                raise UsageError(f"F row {r} is not the pair/obstacle selection of assemble: "
+                                 "unsupported constraint system")
+    G = getattr(sys, "G", None)
+    if G is not None:
+        G = np.asarray(G)
+        if G.shape != (2 * n * K1, n * n_xi):
+            raise UsageError(f"G has shape {G.shape}, expected {(2 * n * K1, n * n_xi)}")
+        for r in sorted({0, K1 - 1, n * K1 - 1, n * K1, 2 * n * K1 - 1}):
+            want = np.zeros(n * n_xi)
+            i, k = (r % (n * K1)) // K1, r % K1
+            want[i * n_xi:(i + 1) * n_xi] = W[k] if r < n * K1 else -W[k]
+            if not np.array_equal(G[r], want):
+                raise UsageError(f"G row {r} is not the workspace box of assemble: "
+                                 "unsupported constraint system")
+
+
 def _system_data(sys, kind: str, rho: float) -> SystemData:
     d = sys.dims
     n, n_d, n_xi, K1, m = d.n, d.n_d, d.n_basis, d.num_steps, d.n_obs
@@ -223,6 +286,7 @@ def _system_data(sys, kind: str, rho: float) -> SystemData:
     W = np.ascontiguousarray(np.asarray(sys.basis.W, float))
     if W.shape != (K1, n_xi):
         raise ShapeError(f"basis W has shape {W.shape}, expected {(K1, n_xi)}")
+    _check_selection_structure(sys, W)
     return SystemData(n=n, n_d=n_d, n_basis=n_xi, num_steps=K1, n_obs=m, n_bnd=nb, W=W,
                       Wdd=np.ascontiguousarray(np.asarray(sys.basis.Wdd, float)),
                       E=np.ascontiguousarray(E), bvals=np.ascontiguousarray(b.reshape(n_d, n, nb)),
@@ -366,16 +430,24 @@ class DeviceBatch:
 
     def __init__(self, systems, xi0, lam0=None, target=None, kind="projection", cfg=None,
                  member_instance=None, early_exit=True, trace=True, counters=False,
-                 device=None, cluster=0, staging=None, copy_stream=None):
+                 device=None, cluster=0, staging=None, copy_stream=None, layout="member"):
         """staging / copy_stream (solve_stream): a caller-owned pinned input arena and the
         stream the input copies are enqueued on (asynchronously); default: the shared
-        staging buffer and synchronous copies."""
+        staging buffer and synchronous copies.
+
+        layout: "member" — xi0 / lam0 / target are (B, n_d, n, n_basis); "producer" — they
+        are (B, n, n_d, n_basis), the layout of the reference's PyTorch producers (the flow
+        sampler, flow_model.py:228-256, and InitNet.forward, init_net.py:74-96). A CUDA
+        tensor in either layout and dtype (FP32 or FP64) is permuted / widened on the
+        device, with no host round trip."""
         import torch
         cfg = cfg or SolverConfig()
         if not isinstance(systems, (list, tuple)):
             systems = [systems]
         if kind not in ("projection", "smoothness"):
             raise UsageError(f"unknown objective kind {kind!r}")
+        if layout not in ("member", "producer"):
+            raise UsageError(f"unknown coefficient layout {layout!r}")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         sds = [system_data(s, kind, cfg.rho) for s in systems]
         sd0 = sds[0]
@@ -393,8 +465,25 @@ class DeviceBatch:
         host_parts, dev_parts, uploaded = [], {}, {}
         direct_bytes = 0
 
+        coeff_names = ("xi0", "lam0", "target")
+
         def add(name, x, shape, dtype=np.float64):
             nonlocal direct_bytes
+            swap = layout == "producer" and name in coeff_names   # (B, n, n_d, c) -> (B, n_d, n, c)
+            if swap:
+                if x.ndim != 4:
+                    raise ShapeError(f"{name} must be (B, n, n_d, n_basis), got {tuple(x.shape)}")
+                if isinstance(x, torch.Tensor):
+                    if x.shape[1:] != (n, n_d, n_xi):
+                        raise ShapeError(f"{name} has shape {tuple(x.shape)}, expected (B, {n}, {n_d}, {n_xi})")
+                    x = x.permute(0, 2, 1, 3)
+                    if not x.is_cuda:
+                        x = x.contiguous()
+                else:
+                    a = np.asarray(x)
+                    if a.shape[1:] != (n, n_d, n_xi):
+                        raise ShapeError(f"{name} has shape {a.shape}, expected (B, {n}, {n_d}, {n_xi})")
+                    x = a.transpose(0, 2, 1, 3)
             if isinstance(x, torch.Tensor) and x.is_cuda:
                 t = x.to(device=dev, dtype=torch.float64 if dtype == np.float64 else torch.int32)
                 dev_parts[name] = t.contiguous()
@@ -526,6 +615,33 @@ class DeviceBatch:
                              p(self.out_its), p(self.out_status), p(self.out_trace),
                              p(self.out_counters))
 
+    def analysis(self, which: str = "xi0"):
+        """The reference's _analyze intermediates (solver.py:158-169) of the batch's input
+        coefficients (which="xi0") or of the solved ones ("xi"), computed on the GPU by
+        sfb_analysis_vars: (SphericalVars, s) in the reference's layouts (batch axis last);
+        s = max(0, h - G xi) is (n_d, 2 n K1, B)."""
+        import torch
+        sd, B = self.sd, self.B
+        n, n_d, K1, m = sd.n, sd.n_d, sd.num_steps, sd.n_obs
+        P = n * (n - 1) // 2
+        dev, f64 = self.device, torch.float64
+        x = (self.xi0 if which == "xi0" else self.out_xi).contiguous()
+        self._wait_launch()
+        Wd = torch.from_numpy(np.ascontiguousarray(sd.W)).to(dev)
+        alpha, beta, dd = (torch.empty((P, K1, B), dtype=f64, device=dev) for _ in range(3))
+        alpha_o, beta_o, d_o = (torch.empty((n, m, K1, B), dtype=f64, device=dev) for _ in range(3))
+        slack = torch.empty((n_d, 2 * n * K1, B), dtype=f64, device=dev)
+        p = lambda t: t.data_ptr() if t.numel() else None
+        stream = torch.cuda.current_stream(dev)
+        rc = _lib.lib().sfb_analysis_vars(
+            x.data_ptr(), B, self.member_instance.data_ptr(), n_d, n, sd.n_basis, K1, m, Wd.data_ptr(),
+            self.pair_axes.data_ptr(), p(self.obs_axes), p(self.obs_pos), self.box.data_ptr(),
+            float(self.d_max), p(alpha), p(beta), p(dd), p(alpha_o), p(beta_o), p(d_o),
+            slack.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
+        _lib.check(rc, "sfb_analysis_vars")
+        h = lambda t: t.cpu().numpy()
+        return SphericalVars(h(alpha), h(beta), h(dd), h(alpha_o), h(beta_o), h(d_o)), h(slack)
+
     def launch_info(self) -> dict:
         """Cluster size, shared memory per CTA and resident CTAs per SM of this batch's launch."""
         c, sm, k = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
@@ -542,12 +658,22 @@ class DeviceBatch:
         rc = _lib.lib().sfb_solve(self.plan.handle, ctypes.byref(self._batch), ctypes.byref(self._cfg),
                                   ctypes.byref(self._out), ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "sfb_solve")
+        # results() copies on the current stream: it waits for this event, so a launch on
+        # any other stream is complete before its outputs are read
+        self._done = torch.cuda.Event()
+        self._done.record(s)
+
+    def _wait_launch(self):
+        import torch
+        ev = getattr(self, "_done", None)
+        if ev is not None:
+            torch.cuda.current_stream(self.device).wait_event(ev)
 
     def results(self) -> dict:
         """Copy results to the host (synchronizes): one copy of the output arena (the trace
         only up to the longest member's iterations). Member-major arrays."""
-        import torch
         B, n_d, n, n_xi = self.out_xi.shape
+        self._wait_launch()
         # a small arena (the latency case) crosses in one copy with the whole trace; a large
         # one copies the head first, then the trace only up to the longest member's iterations
         one_copy = self.out_trace is not None and self._out_arena.numel() * 8 <= SMALL_D2H_BYTES
@@ -645,7 +771,9 @@ def solve(init: SolverState, sys, mode: ObjectiveMode, cfg: SolverConfig | None 
 
 def fixed_point_step(state: SolverState, sys, mode: ObjectiveMode, cfg: SolverConfig,
                      cache: KktCache | None = None) -> SolverState:
-    """solver.py:246-256: one map application (run as a 1-iteration fixed solve)."""
+    """solver.py:246-256: one map application (run as a 1-iteration fixed solve). Like the
+    reference, the returned state carries the slack `s` (n_d, g_rows, B) and the spherical
+    variables `vars` of the INPUT iterate (computed on the GPU, sfb_analysis_vars)."""
     B = state.batch_size
     d = sys.dims
     kind = getattr(mode, "kind", None)
@@ -660,9 +788,10 @@ def fixed_point_step(state: SolverState, sys, mode: ObjectiveMode, cfg: SolverCo
                         kind=kind, cfg=one, early_exit=False, trace=False)
     batch.launch()
     out = batch.results()
+    vars_, s = batch.analysis("xi0")
     xi = np.moveaxis(out["xi"].reshape(B, d.n_d, d.nvar_ax), 0, -1)
     lam = np.moveaxis(out["lam"].reshape(B, d.n_d, d.nvar_ax), 0, -1)
-    return SolverState(xi=xi, lam=lam, iteration=state.iteration + 1)
+    return SolverState(xi=xi, lam=lam, s=s, vars=vars_, iteration=state.iteration + 1)
 
 
 @dataclass
@@ -682,7 +811,7 @@ class BatchResult:
 def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projection",
                     cfg: SolverConfig | None = None, member_instance=None,
                     fixed_iterations: bool = False, trace: bool = True,
-                    cluster: int = 0) -> BatchResult:
+                    cluster: int = 0, layout: str = "member") -> BatchResult:
     """Solve instances x samples in one launch (host arrays in, host arrays out).
 
     xi0/lam0/target: (B, n_d, n, n_basis) (numpy or torch, host or device);
@@ -690,12 +819,14 @@ def solve_instances(systems, xi0, lam0=None, target=None, kind: str = "projectio
     fixed_iterations=True every member runs exactly cfg.max_iters + 1 map
     evaluations (the throughput protocol of SURVEY.md §8(d)). `cluster` = CTAs per
     member (0: auto — batches too small to fill the GPU split each member over a
-    thread-block cluster for latency)."""
+    thread-block cluster for latency). layout="producer": the coefficients are
+    (B, n, n_d, n_basis) as the reference's sampler / init network emit them (see
+    DeviceBatch); results are member-major either way."""
     cfg = cfg or SolverConfig()
     t0 = time.perf_counter()
     batch = DeviceBatch(systems, xi0, lam0, target, kind=kind, cfg=cfg,
                         member_instance=member_instance, early_exit=not fixed_iterations,
-                        trace=trace, cluster=cluster)
+                        trace=trace, cluster=cluster, layout=layout)
     batch.launch()
     out = batch.results()
     return BatchResult(xi=out["xi"], lam=out["lam"], status=out["status"],

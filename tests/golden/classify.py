@@ -34,8 +34,12 @@ OVERRIDE = {"known_coincident": "lam_degenerate"}
 
 
 def main():
-    manifest = {}
+    # names on the command line: (re)classify those only and merge into the manifest
+    only = set(sys.argv[1:])
+    manifest = golden_io.manifest() if only else {}
     for name in golden_io.names():
+        if only and name not in only:
+            continue
         g = golden_io.load(name)
         fixed = all(s == "max_iters" for s in g.out["status"])
         kw = dict(kind=g.kind, target=g.target, rho=g.rho, max_iters=g.max_iters,

@@ -146,6 +146,36 @@ def main():
     run("c4_inst0_L2", scn, B100, xi, lam, "projection", SolverConfig(max_iters=2, **FIXED),
         note="BASELINE configs[3] instance 0, L=2")
 
+    # The benched configuration itself: C3 instance 0 (8 samples) over the full L=500 of
+    # the throughput protocol (~25 min of reference time on one core), the C2 drift-stress
+    # case over L=500, C4 over L=100, and two C3 instances at the same L so the GPU test
+    # can solve them in ONE launch with an interleaved member->instance map.
+    scn = generate(fam(20, 2.0), 32, 2, seed=3000, horizon=b100)
+    xi, lam = naive(scn, B100, 8, seed=3000)
+    run("c3_inst0_L500", scn, B100, xi, lam, "projection", SolverConfig(max_iters=500, **FIXED),
+        note="BASELINE configs[2] instance 0 (8 samples), the benched L=500")
+    scn = generate(fam(10, 1.0), 16, 2, seed=2001, horizon=b100)
+    xi, lam = naive(scn, B100, 4, seed=2001)
+    run("c2_inst0_L500", scn, B100, xi, lam, "projection", SolverConfig(max_iters=500, **FIXED),
+        note="16/10 in [-1,1], L=500: the FP-drift stress case at the full iteration count")
+    scn = generate(fam(30, 2.0), 64, 2, seed=4000, horizon=b100)
+    xi, lam = naive(scn, B100, 1, seed=4000)
+    run("c4_inst0_L100", scn, B100, xi, lam, "projection", SolverConfig(max_iters=100, **FIXED),
+        note="BASELINE configs[3] instance 0, L=100")
+    for i in (0, 1):
+        scn = generate(fam(20, 2.0), 32, 2, seed=3100 + i, horizon=b100)
+        xi, lam = naive(scn, B100, 4, seed=3100 + i, lam_scale=0.3, lam_seed=3100 + i)
+        run(f"c3pair_inst{i}_L40", scn, B100, xi, lam, "projection",
+            SolverConfig(max_iters=40, **FIXED),
+            note="one of two C3 instances solved together in one launch by the GPU test")
+    # a batch whose members stop on different predicates: member 1 on the fixed-point
+    # residual (converged_fp, solver.py:320-322), the others on the primal residual
+    scn = generate(fam(3, 1.5), 8, 2, seed=11, horizon=B50.config)
+    xi, lam = naive(scn, B50, 3, seed=11)
+    run("fp_converge_obs8", scn, B50, xi, lam, "projection",
+        SolverConfig(max_iters=20000, primal_tol=1e-9, fp_tol=1e-8),
+        note="member 1 ends converged_fp at iteration 290")
+
     # obstacles, smoothness, rho, rest_to_rest, 3D, moving obstacles
     scn = generate(fam(3, 1.5), 8, 2, seed=11, horizon=B50.config)
     xi, lam = naive(scn, B50, 3, seed=11, lam_scale=0.3)

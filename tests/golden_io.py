@@ -36,9 +36,10 @@ class Golden:
 
 
 def names():
-    """Solver fixtures (metrics_*.npz / plan_*.npz belong to the epilogue and planner tests)."""
+    """Solver fixtures (metrics_*.npz / plan_*.npz / stepvars_*.npz belong to the epilogue,
+    planner and fixed_point_step-analysis tests)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if not os.path.basename(p).startswith(("metrics_", "plan_")))
+                  if not os.path.basename(p).startswith(("metrics_", "plan_", "stepvars_")))
 
 
 def load(name: str) -> Golden:
@@ -95,11 +96,15 @@ def compare(got: dict, ref: dict):
     """Worst-case errors between two solve outputs (member-major dicts).
 
     xi_rel: per member max|dxi| / max|xi_ref|; lam_abs; primal/trace abs.
+    fp_abs / fp_rel: the fixed-point column trace[:, 1] (solver.py:316, 329-333):
+    absolute error and error relative to max(|fp_ref|, 1e-12) over the finite
+    entries; the first entry (+inf, before any step) must be +inf on both sides.
     In fixed-iteration mode iterations and status must match exactly."""
     B = len(ref["iterations"])
     flat = lambda v: np.asarray(v).reshape(-1)
-    xi_rel = lam_abs = trace_abs = final_abs = eq_abs = 0.0
+    xi_rel = lam_abs = trace_abs = final_abs = eq_abs = fp_abs = fp_rel = 0.0
     same_its = True
+    fp_inf_ok = True
     for b in range(B):
         xr = flat(ref["xi"][b])
         xi_rel = max(xi_rel, float(np.abs(flat(got["xi"][b]) - xr).max()
@@ -108,9 +113,18 @@ def compare(got: dict, ref: dict):
         tg, tr = np.asarray(got["trace"][b]), np.asarray(ref["trace"][b])
         L = min(len(tg), len(tr))
         trace_abs = max(trace_abs, float(np.abs(tg[:L, 0] - tr[:L, 0]).max()))
+        if L:
+            fp_inf_ok &= bool(np.isposinf(tg[0, 1]) and np.isposinf(tr[0, 1]))
+        if L > 1:
+            fg, fr = tg[1:L, 1], tr[1:L, 1]
+            fp_inf_ok &= bool(np.all(np.isfinite(fg)) and np.all(np.isfinite(fr)))
+            dfp = np.abs(fg - fr)
+            fp_abs = max(fp_abs, float(dfp.max()))
+            fp_rel = max(fp_rel, float((dfp / np.maximum(np.abs(fr), 1e-12)).max()))
         final_abs = max(final_abs, abs(float(got["primal"][b]) - float(ref["primal"][b])))
         eq_abs = max(eq_abs, abs(float(got["eq_max"][b]) - float(ref["eq_max"][b])))
         same_its &= int(got["iterations"][b]) == int(ref["iterations"][b]) and \
             got["status"][b] == ref["status"][b]
     return dict(xi_rel=xi_rel, lam_abs=lam_abs, trace_abs=trace_abs, final_abs=final_abs,
-                eq_abs=eq_abs, same_iterations=same_its)
+                eq_abs=eq_abs, same_iterations=same_its, fp_abs=fp_abs, fp_rel=fp_rel,
+                fp_inf_ok=fp_inf_ok)

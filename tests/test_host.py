@@ -133,3 +133,31 @@ def test_kron_structure_check_matches_dense_kronecker():
             dense = bool(np.array_equal(B, np.kron(np.eye(n), E)))
             assert solver._kron_checked(B, n, E) == dense
         assert not solver._kron_checked(A[:, :-1], n, E)                 # wrong shape
+
+
+def test_dense_selection_structure_is_checked():
+    """a system carrying dense F / G / pair_index (the reference's
+    ConstraintSystem) is checked against the structure the Kronecker plan assumes."""
+    import dataclasses
+    from oracle import sf_dense
+    g = golden_io.load("obs8_projection")
+    d = g.sys.dims
+    F, G, pairs = sf_dense.dense_operators(d.n, d.n_obs, g.sys.basis.W)
+    ok = dataclasses.replace(g.sys, F=F, G=G)
+    solver._system_data(ok, "projection", 1.0)          # the assemble structure passes
+    rows = {0, d.num_steps - 1, d.n_pairs * d.num_steps - 1, d.n_pairs * d.num_steps,
+            F.shape[0] - 1, (d.n_pairs // 2) * d.num_steps + d.num_steps // 2}
+    F2 = F.copy()
+    F2[sorted(rows)[2]] *= 2.0                            # a re-weighted (sampled) pair row
+    with pytest.raises(UsageError):
+        solver._system_data(dataclasses.replace(g.sys, F=F2, G=G), "projection", 1.0)
+    with pytest.raises(UsageError):                      # missing obstacle rows
+        solver._system_data(dataclasses.replace(g.sys, F=F[:-d.num_steps], G=G), "projection", 1.0)
+    with pytest.raises(UsageError):                      # a box of different sign
+        solver._system_data(dataclasses.replace(g.sys, F=F, G=-G), "projection", 1.0)
+
+    import types
+    w = types.SimpleNamespace(**{f.name: getattr(g.sys, f.name) for f in dataclasses.fields(g.sys)},
+                              pair_index=[(0, 1)])              # a subset of the pairs
+    with pytest.raises(UsageError):
+        solver._system_data(w, "projection", 1.0)
