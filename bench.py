@@ -12,8 +12,11 @@ One step = one SF solve of the rank's whole batch. `value` is timed on the devic
 (CUDA events around the kernel, inputs resident in HBM, L2 flushed between steps);
 `e2e` goes through the public serving API `solve_stream` with host inputs (every step
 packs and copies its inputs H2D and reads its outputs D2H inside the timed region; the
-copies overlap the neighbouring steps' kernels). `--impl reference` times the reference algorithm
-(oracle/sf_dense.py, the faithful dense restatement) on the host cores instead.
+copies overlap the neighbouring steps' kernels; the e2e case is the reference planner's default
+warm start, xi0 = target = the samples, lambda0 = 0, pipeline.py:123-124, so the samples cross
+PCIe once). `--impl reference` times the reference algorithm (oracle/sf_dense.py, the
+operation-for-operation port; the reference package cannot travel to the GPU box) on the host
+cores instead.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -143,40 +146,42 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU legs
-_CPU_STATE = {}
+# The reference SF is numpy/scipy (pkg/src/swarmplan/solver.py:286-355); it cannot travel to
+# the GPU box, so both CPU legs time oracle/sf_dense.py, its operation-for-operation port
+# (dense F / G einsums, arctan2 / sin / cos, scipy LU), pinned to the reference's own outputs
+# at ~1e-13 (tests/test_oracle.py). Protocol (reference harness
+# bench.py:74-145): W worker processes with one BLAS thread each; worker w builds instance w
+# (all S samples, setup = assemble + dense F + KKT LU, reported separately) ONCE; every step
+# releases all workers together through a barrier, each runs L_cpu + 1 map evaluations of
+# its instance, and the step time is the slowest worker's; per-evaluation cost is constant
+# in fixed-iteration mode, so instances/s extrapolates linearly to L = 500.
 
 
-def _cpu_init(wl, L_cpu):
-    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
-    _CPU_STATE["wl"] = wl
-    _CPU_STATE["L"] = L_cpu
-
-
-def _cpu_task(i):
-    """One instance (all S samples) through the faithful dense restatement of the
-    reference solve_batch (oracle/sf_dense.py); returns (setup_s, solve_s, evals)."""
+def _cpu_worker(idx, wl, L, nsteps, barrier, q):
     from oracle import sf_dense
     from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble, build_basis,
                                                generate, sample_naive_prior, stack_xi)
-    wl, L = _CPU_STATE["wl"], _CPU_STATE["L"]
-    basis = build_basis(BasisConfig(wl["n_basis"], wl["K1"], wl["duration"]))
-    fam = ScenarioFamily("random_box", robot_radius=wl["robot_radius"], box=(-wl["h"], wl["h"]),
-                         n_obstacles=wl["m"], obstacle_radius=wl["obstacle_radius"])
-    seed = 3000 + i
-    cached = _CPU_STATE.get(("sf", i))
-    t0 = time.perf_counter()
-    if cached is None:
+    try:
+        t0 = time.perf_counter()
+        basis = build_basis(BasisConfig(wl["n_basis"], wl["K1"], wl["duration"]))
+        fam = ScenarioFamily("random_box", robot_radius=wl["robot_radius"], box=(-wl["h"], wl["h"]),
+                             n_obstacles=wl["m"], obstacle_radius=wl["obstacle_radius"])
+        seed = 3000 + idx
         scn = generate(fam, wl["n"], 2, seed=seed, horizon=basis.config)
         sys_ = assemble(scn, basis)
         xi = stack_xi(sample_naive_prior(scn, basis, wl["samples"], seed=seed))
         sf = sf_dense.DenseSF(sys_, "projection", 1.0)
-        _CPU_STATE[("sf", i)] = cached = (sys_, xi, sf)
-    sys_, xi, sf = cached
-    t1 = time.perf_counter()
-    sf_dense.solve_batch(sys_, xi, np.zeros_like(xi), kind="projection", target=xi, max_iters=L,
-                         primal_tol=1e-300, fp_tol=1e-300, sf=sf)
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t1, wl["samples"] * (L + 1)
+        lam = np.zeros_like(xi)
+        q.put(("setup", idx, time.perf_counter() - t0))
+    except Exception as exc:   # pragma: no cover - reported to the parent
+        q.put(("error", idx, repr(exc)))
+        return
+    for step in range(nsteps):
+        barrier.wait()
+        t1 = time.perf_counter()
+        sf_dense.solve_batch(sys_, xi, lam, kind="projection", target=xi, max_iters=L,
+                             primal_tol=1e-300, fp_tol=1e-300, sf=sf)
+        q.put(("solve", idx, time.perf_counter() - t1))
 
 
 def cpu_workers():
@@ -190,51 +195,106 @@ def cpu_workers():
     return max(1, min(n, 64))
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 class CpuReference:
-    """Pool of W processes, one instance per process and step."""
+    """W synchronized worker processes, one fixed instance each."""
 
-    def __init__(self, L_cpu=2, workers=None):
+    def __init__(self, L_cpu=5, steps=1, warmup=1, workers=None):
         self.W = workers or cpu_workers()
-        self.L = L_cpu
-        ctx = mp.get_context("fork")
-        self.pool = ctx.Pool(self.W, initializer=_cpu_init, initargs=(WL, L_cpu))
+        self.L, self.steps, self.warmup = L_cpu, steps, warmup
+        ctx = mp.get_context("spawn")        # children never touch CUDA or the parent's threads
+        self.barrier = ctx.Barrier(self.W + 1)
+        self.q = ctx.Queue()
+        keep = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+        os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+        try:
+            self.procs = [ctx.Process(target=_cpu_worker,
+                                      args=(i, WL, L_cpu, warmup + steps, self.barrier, self.q), daemon=True)
+                          for i in range(self.W)]
+            for p in self.procs:
+                p.start()
+        finally:
+            for k, v in keep.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        setups = []
+        for _ in range(self.W):
+            kind, idx, val = self.q.get(timeout=1800)
+            if kind == "error":
+                raise RuntimeError(f"CPU worker {idx}: {val}")
+            setups.append(val)
+        self.setup_s = statistics.median(setups)
 
-    def step(self):
-        t0 = time.perf_counter()
-        res = self.pool.map(_cpu_task, range(self.W), chunksize=1)
-        wall = time.perf_counter() - t0
-        setup = max(r[0] for r in res)
-        solve = max(r[1] for r in res)
-        evals = sum(r[2] for r in res)
-        # instances/s at L = WL["L"]: member-evaluations per second / evaluations per instance
+    def _step(self):
+        self.barrier.wait()
+        times = [self.q.get(timeout=1800)[2] for _ in range(self.W)]
+        solve = max(times)
+        evals = self.W * WL["samples"] * (self.L + 1)
         per_inst = WL["samples"] * (WL["L"] + 1)
-        return {"inst_per_s": evals / solve / per_inst, "wall": wall, "setup_s": setup,
-                "solve_s": solve, "evals": evals}
+        return {"inst_per_s": evals / solve / per_inst, "solve_s": solve,
+                "spread": (max(times) - min(times)) / max(times)}
+
+    def run(self):
+        for _ in range(self.warmup):
+            self._step()
+        res = [self._step() for _ in range(self.steps)]
+        for p in self.procs:
+            p.join(timeout=60)
+        return res
 
     def close(self):
-        self.pool.terminate()
+        for p in self.procs:
+            if p.is_alive():
+                p.terminate()
 
-    def describe(self):
-        return {"cores": self.W, "kind": "port",
-                "sample": (f"{self.W} instances in parallel (1 per process, 1 thread each), "
-                           f"{WL['samples']} samples x {self.L + 1} map evaluations each through "
-                           f"oracle/sf_dense.py (dense-F restatement of solver.py:286-355), "
-                           f"extrapolated to L={WL['L']} (per-iteration cost is constant); "
-                           f"setup (F, F^T F, LU) excluded like the GPU plan")}
+    def describe(self, res):
+        v = [r["inst_per_s"] for r in res]
+        return {"cores": self.W, "kind": "port", "cpu_model": cpu_model(),
+                "threads": "1 BLAS/OpenMP thread per process",
+                "sample": (f"{self.W} instances in parallel (one fixed instance per process, built once; "
+                           f"workers released together by a barrier each step), {WL['samples']} samples x "
+                           f"{self.L + 1} map evaluations per instance and step through oracle/sf_dense.py "
+                           f"(the operation-for-operation port of the reference solve_batch, "
+                           f"solver.py:286-355; the reference package itself cannot travel to the GPU box), "
+                           f"{self.warmup} warm-up + {self.steps} timed steps, extrapolated to L={WL['L']} "
+                           f"(per-evaluation cost is constant); setup (F, F^T F, LU) excluded like the GPU plan"),
+                "median": statistics.median(v), "min": min(v), "max": max(v),
+                "setup_s_per_instance": self.setup_s}
+
+
+def cpu_iters_for_budget(steps, warmup, budget_s=240.0, eval_s=3.1, want=5):
+    """L_cpu for the reference arm: BASELINE.md §3's 5 when the whole run fits `budget_s`
+    (one C3 evaluation of 8 samples ~3 s on one core), fewer otherwise (>= 1)."""
+    fit = int(budget_s / max(1, steps + warmup) / eval_s) - 1
+    return max(1, min(want, fit))
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    ref = CpuReference(L_cpu=args.cpu_iters)
-    for _ in range(args.warmup):
-        ref.step()
-    vals = [ref.step() for _ in range(args.steps)]
-    ref.close()
-    v = statistics.mean(r["inst_per_s"] for r in vals)
-    ms = statistics.mean(r["solve_s"] for r in vals) * 1e3
-    desc = ref.describe()
+    L = args.cpu_iters if args.cpu_iters > 0 else cpu_iters_for_budget(args.steps, args.warmup)
+    ref = CpuReference(L_cpu=L, steps=args.steps, warmup=args.warmup)
+    try:
+        vals = ref.run()
+    finally:
+        ref.close()
+    desc = ref.describe(vals)
+    v = desc["median"]
+    ms = statistics.median(r["solve_s"] for r in vals) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -242,7 +302,7 @@ def run_reference_arm(args):
         "config": config_dict(args.gpus),
         "cpu_baseline": {"value": v, "unit": "instances/s", **desc},
         "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "setup_s_per_instance": statistics.mean(r["setup_s"] for r in vals),
+        "setup_s_per_instance": desc["setup_s_per_instance"],
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -403,11 +463,13 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        ref = CpuReference(L_cpu=args.cpu_iters)
-        r = ref.step()
-        ref.close()
-        cpu = {"value": r["inst_per_s"], "unit": "instances/s", **ref.describe(),
-               "setup_s_per_instance": r["setup_s"]}
+        ref = CpuReference(L_cpu=args.cpu_iters if args.cpu_iters > 0 else 5, steps=2, warmup=1)
+        try:
+            vals = ref.run()
+        finally:
+            ref.close()
+        desc = ref.describe(vals)
+        cpu = {"value": desc["median"], "unit": "instances/s", **desc}
 
     if rank == 0:
         line = {
@@ -437,7 +499,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--cpu-iters", type=int, default=2, help="fixed iterations per CPU sample")
+    ap.add_argument("--cpu-iters", type=int, default=0,
+                    help="fixed iterations per CPU sample (0: 5, fewer in the reference arm if "
+                         "--steps/--warmup would exceed ~4 min)")
     ap.add_argument("--latency", type=int, default=100, help="distinct instances for the p50 latency (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":

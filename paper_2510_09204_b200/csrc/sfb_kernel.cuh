@@ -87,6 +87,13 @@ struct KParams {
   int* status;
   double* trace;
   unsigned long long* counters;
+  // split schedule (csize == 1, more members than resident CTAs): the grid is one wave of
+  // persistent CTAs and CTA c runs evaluation units [c U / G, (c + 1) U / G) of the
+  // member-major unit list (U = B (max_iters + 1)); a member cut at a unit boundary is handed
+  // from CTA c to CTA c + 1 through hand_flag[c] / hand[c] (and the member's xi / lam outputs)
+  int split;
+  unsigned* hand_flag;   // [G] 0 = pending, 1 = handed over, 2 = member already finished
+  double* hand;          // [G][2 * nt] per-thread fixed-point partial and boundary-residual max
 };
 
 // plan constant block offsets (doubles)
@@ -233,8 +240,14 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
 // BIG2 (n = 33..64, 2D): the n > 32 kernel capped at 128 registers, 8-warp CTAs, two per SM
 // (16 warps per SM; the uncapped build needs 230 registers and runs 4-warp CTAs)
+// One member's solve, evaluations it0 .. (max_iters or convergence), by one CTA (or one cluster).
+// hand_in >= 0: the member's state after evaluation it0 - 1 comes from the split-schedule
+// handoff slot hand_in (xi / lambda in the member's outputs); it_stop >= 0: stop before
+// evaluation it_stop and leave the state in handoff slot hand_out. Returns true when the
+// member finished (converged or reached max_iters) and its outputs are written.
 template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
-__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {  // @stage setup
+__device__ __forceinline__ bool sf_member(const KParams& P, const int b, const int it0, const int it_stop,
+                                          const int hand_in, const int hand_out) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
@@ -245,7 +258,6 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // of the k-group tasks and all ranks run the (identical) KKT step redundantly
   const int csize = P.csize;
   const int crank = csize > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
-  const int b = blockIdx.x / csize;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = BIG ? P.nw : NW, nt = nw * 32;   // n <= 32 always runs NW warps (compile-time strides)
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
@@ -336,13 +348,16 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     }
   }
   {
-    const double* x0 = P.xi0 + (size_t)b * nv;
-    const double* l0 = P.lam0 + (size_t)b * nv;
+    // a handed-over member resumes from the iterate its previous CTA left in the outputs
+    // (written by another SM in this launch: read through L2)
+    const bool resume = hand_in >= 0;
+    const double* x0 = (resume ? P.xi : P.xi0) + (size_t)b * nv;
+    const double* l0 = (resume ? P.lam : P.lam0) + (size_t)b * nv;
     const double* t0 = P.target ? P.target + (size_t)b * nv : nullptr;
     for (int o = tid; o < nv; o += nt) {
       const int ai = o / NXI, c = o - ai * NXI;
-      sXi[ai * NXP + c] = x0[o];
-      sLam[ai * NXP + c] = l0[o];
+      sXi[ai * NXP + c] = resume ? __ldcg(x0 + o) : x0[o];
+      sLam[ai * NXP + c] = resume ? __ldcg(l0 + o) : l0[o];
       sTgt[o] = t0 ? t0[o] : 0.0;
     }
   }
@@ -521,10 +536,32 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   double eq_max = 0.0, eql = 0.0;
   double fpp = 0.0;   // per-lane ||dlambda||^2 + ||dxi||^2 partial of the last KKT step
+  if (hand_in >= 0) {   // the per-thread carries of the previous CTA (same thread, same values)
+    const double* hb = P.hand + (size_t)hand_in * 2 * nt;
+    fpp = __ldcg(hb + tid);
+    eql = __ldcg(hb + nt + tid);
+  }
+  bool finished = true;
   // per-thread counts fit 32 bits (rows of one lane over one solve); summed in 64 bits at the end
   unsigned c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
-  for (int it = 0;; ++it) {  // @stage iter_top
+  for (int it = it0;; ++it) {  // @stage iter_top
+    if (it == it_stop) {
+      // split schedule: hand the state before evaluation it to the next CTA (xi / lambda
+      // through the member's outputs, the per-thread carries through the handoff slot)
+      double* xo = P.xi + (size_t)b * nv;
+      double* lo = P.lam + (size_t)b * nv;
+      for (int o = tid; o < nv; o += nt) {
+        const int ai = o / NXI, c = o - ai * NXI;
+        xo[o] = sXi[ai * NXP + c];
+        lo[o] = sLam[ai * NXP + c];
+      }
+      double* hb = P.hand + (size_t)hand_out * 2 * nt;
+      hb[tid] = fpp;
+      hb[nt + tid] = eql;
+      finished = false;
+      break;
+    }
     // -------------------------------------------- A/B/C per k-group task
     // G partials (not TBL): the first RA axes in registers, the rest in per-lane smem slots
     constexpr int RA = BIG ? ND : (SFB_GREG > ND ? ND : SFB_GREG);
@@ -1509,6 +1546,66 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
       atomicAdd(cb + 1, w_active);
       atomicAdd(cb + 2, w_screen);
       if (warp == 0 && crank == 0) atomicAdd(cb + 3, (unsigned long long)c_evals);
+    }
+  }
+  return finished;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
+__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {
+  // Split schedule ("stream-K" over evaluation units): with B > G resident CTAs, one CTA per
+  // member would leave the last of ceil(B / G) waves partly idle (C3: 512 members on 296
+  // slots = 1.73 waves of work in 2). Instead the G CTAs form one cooperative wave and CTA c
+  // runs units [c U / G, (c + 1) U / G), U = B E, E = max_iters + 1. Since B >= G every range
+  // holds at least E units, so at most two members are cut: the range's LAST member (its
+  // head, evaluations [0, rb)) runs FIRST and is handed to CTA c + 1, whose range starts
+  // with that member's tail, run LAST — by then the head (started at time 0 and no longer
+  // than a range) is done, so a CTA does not wait in a balanced wave. Every evaluation runs
+  // the same code on the same state, so results are bitwise those of the unsplit launch.
+  // Pieces of this CTA in order: [head of mb] [full members] [tail of ma]; one call site of
+  // the (large, inlined) member solve.
+  int ma = 0, ra = 0, mb = 0, rb = 0, first = blockIdx.x / P.csize, npieces = 1;
+  const int c = blockIdx.x;
+  if (P.split) {
+    const long long E = (long long)P.max_iters + 1, U = (long long)P.B * E, G = gridDim.x;
+    const long long lo = c * U / G, hi = (c + 1) * U / G;
+    ma = (int)(lo / E); ra = (int)(lo % E); mb = (int)(hi / E); rb = (int)(hi % E);
+    first = ra ? ma + 1 : ma;
+    npieces = (rb ? 1 : 0) + (mb - first) + (ra ? 1 : 0);
+  }
+  for (int piece = 0; piece < npieces; ++piece) {
+    int b, it0 = 0, it_stop = -1, hand_in = -1, hand_out = -1;
+    if (P.split && rb && piece == 0) {            // head of mb, handed to CTA c + 1
+      b = mb;
+      it_stop = rb;
+      hand_out = c;
+    } else if (P.split && ra && piece == npieces - 1) {   // tail of ma, from CTA c - 1
+      b = ma;
+      it0 = ra;
+      hand_in = c - 1;
+      unsigned f = 0u;
+      if (threadIdx.x == 0) {
+        while ((f = ld_acquire_gpu(P.hand_flag + c - 1)) == 0u) __nanosleep(256);
+      }
+      // the member may have converged inside the head: nothing left to do
+      if (__syncthreads_or(f == 2u)) continue;
+    } else {
+      b = first + piece - ((P.split && rb) ? 1 : 0);
+    }
+    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2>(P, b, it0, it_stop, hand_in, hand_out);
+    __syncthreads();                              // shared memory reused by the next piece; handoff stores issued
+    if (hand_out >= 0 && threadIdx.x == 0) {
+      __threadfence();
+      st_release_gpu(P.hand_flag + c, fin ? 2u : 1u);
     }
   }
 }
