@@ -135,13 +135,6 @@ __device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __
 
 // 1/sqrt(q) in FP64 from the FP32 MUFU seed and one Newton step (relative error ~1e-14,  // @stage exact_math
 // vs ~1e-16 for rsqrt(double); the seed needs q inside the FP32 normal range)
-__device__ __forceinline__ double rsqrt_fast(double q) {
-  if (!(q > 1e-30 && q < 1e30)) return rsqrt(q);
-  const double y = (double)rsqrtf((float)q);
-  return y * fma(-0.5 * q, y * y, 1.5);
-}
-
-// the same for q in (0, 1): only underflow of the FP32 seed needs the slow path
 __device__ __forceinline__ double rsqrt_fast01(double q) {
   if (!(q > 1e-30)) return rsqrt(q);
   const double y = (double)rsqrtf((float)q);
@@ -150,6 +143,7 @@ __device__ __forceinline__ double rsqrt_fast01(double q) {
 
 // Exact FP64 residual of one separation row (constraints.py:166-247, trig-free):
 // r1 = delta * (1 - clip(rho, 1, d_max) / rho), coincident rows use alpha = 0, beta = pi/2.
+// Returns false (r untouched) on the inactive range 1 <= rho <= d_max.
 template <int ND>
 __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, double inv_b2,
                                           double ax_a, double ax_b, double d_max,
@@ -895,18 +889,18 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
             }
           };
           if (merge) {
+            // one loop over a lane's pair bits, then its obstacle bits; the body is branch-free
+            // apart from the row math's rare slow path (partner position and row parameters
+            // by select), so a pass costs the same for pair and obstacle rows
             unsigned pmk = pdef, omk = mask;
+            const double pia2 = sKD[KC_INV_A2], pib2 = sKD[KC_INV_B2], pa = sKD[KC_RA], pb = sKD[KC_RB];
             while (__any_sync(FULL, (pmk | omk) != 0u)) {
               const bool isp = pmk != 0u;
               const bool act = isp || omk != 0u;
-              int jl = 0, o = 0;
-              if (isp) {
-                jl = __ffs(pmk) - 1;
-                pmk &= pmk - 1u;
-              } else if (act) {
-                o = __ffs(omk) - 1;
-                omk &= omk - 1u;
-              }
+              const int bit = __ffs(isp ? pmk : omk) - 1;          // -1: no row left
+              pmk = isp ? (pmk & (pmk - 1u)) : pmk;
+              omk = isp ? omk : (omk & (omk - 1u));
+              const int jl = isp ? bit : 0, o = isp ? 0 : max(bit, 0);
               double pj[ND][2];
               if (__any_sync(FULL, isp)) {
                 const int src = sub * LW + jl;
@@ -915,38 +909,32 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
 #pragma unroll
                   for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
               }
-              if (act) {
-                double ia2 = sKD[KC_INV_A2], ib2 = sKD[KC_INV_B2], aa = sKD[KC_RA], bb = sKD[KC_RB];
-                double cs = (i < jl) ? 1.0 : -1.0;
-                if (!isp) {
-                  const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
-                  ia2 = ax.x;
-                  ib2 = ax.y;
-                  aa = ax.z;
-                  bb = ax.w;
-                  cs = 1.0;
+              const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
+              if (!isp) {
 #pragma unroll
-                  for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
-                }
-                const bool once = !isp || i < jl;   // rows the reference's F holds once
+                for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
+              }
+              const double ia2 = isp ? pia2 : ax.x, ib2 = isp ? pib2 : ax.y;
+              const double aa = isp ? pa : ax.z, bb = isp ? pb : ax.w;
+              const double cs = (!isp || i < jl) ? 1.0 : -1.0;
+              const bool once = !isp || i < jl;   // rows the reference's F holds once
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                  if (kk < nsteps) {
-                    double d[ND], r[ND];
+              for (int kk = 0; kk < 2; ++kk) {
+                if (act && kk < nsteps) {
+                  double d[ND], r[ND];
 #pragma unroll
-                    for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
-                    ++c_exact;
-                    if (row_exact<ND>(d, ia2, ib2, aa, bb, sKD[KC_DMAX], cs, r)) {
-                      double rr = 0.0;
+                  for (int a = 0; a < ND; ++a) d[a] = p[a][kk] - pj[a][kk];
+                  ++c_exact;
+                  if (row_exact<ND>(d, ia2, ib2, aa, bb, sKD[KC_DMAX], cs, r)) {
+                    double rr = 0.0;
 #pragma unroll
-                      for (int a = 0; a < ND; ++a) {
-                        g[a][kk] += r[a];
-                        rr = fma(r[a], r[a], rr);
-                      }
-                      if (once) {
-                        ++c_active;
-                        s1 += rr;
-                      }
+                    for (int a = 0; a < ND; ++a) {
+                      g[a][kk] += r[a];
+                      rr = fma(r[a], r[a], rr);
+                    }
+                    if (once) {
+                      ++c_active;
+                      s1 += rr;
                     }
                   }
                 }
