@@ -157,7 +157,7 @@ class Clocks:
 # in fixed-iteration mode, so instances/s extrapolates linearly to L = 500.
 
 
-def _cpu_worker(idx, wl, L, nsteps, barrier, q):
+def _cpu_worker(idx, wl, L, nsteps, barrier, q, seed0=3000):
     from oracle import sf_dense
     from paper_2510_09204_b200.problem import (BasisConfig, ScenarioFamily, assemble, build_basis,
                                                generate, sample_naive_prior, stack_xi)
@@ -166,7 +166,7 @@ def _cpu_worker(idx, wl, L, nsteps, barrier, q):
         basis = build_basis(BasisConfig(wl["n_basis"], wl["K1"], wl["duration"]))
         fam = ScenarioFamily("random_box", robot_radius=wl["robot_radius"], box=(-wl["h"], wl["h"]),
                              n_obstacles=wl["m"], obstacle_radius=wl["obstacle_radius"])
-        seed = 3000 + idx
+        seed = seed0 + idx
         scn = generate(fam, wl["n"], 2, seed=seed, horizon=basis.config)
         sys_ = assemble(scn, basis)
         xi = stack_xi(sample_naive_prior(scn, basis, wl["samples"], seed=seed))
@@ -210,7 +210,8 @@ def cpu_model():
 class CpuReference:
     """W synchronized worker processes, one fixed instance each."""
 
-    def __init__(self, L_cpu=5, steps=1, warmup=1, workers=None):
+    def __init__(self, L_cpu=5, steps=1, warmup=1, workers=None, wl=None, seed0=3000):
+        self.wl = wl = dict(WL if wl is None else wl)
         self.W = workers or cpu_workers()
         self.L, self.steps, self.warmup = L_cpu, steps, warmup
         ctx = mp.get_context("spawn")        # children never touch CUDA or the parent's threads
@@ -220,7 +221,8 @@ class CpuReference:
         os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
         try:
             self.procs = [ctx.Process(target=_cpu_worker,
-                                      args=(i, WL, L_cpu, warmup + steps, self.barrier, self.q), daemon=True)
+                                      args=(i, wl, L_cpu, warmup + steps, self.barrier, self.q, seed0),
+                                      daemon=True)
                           for i in range(self.W)]
             for p in self.procs:
                 p.start()
@@ -242,8 +244,8 @@ class CpuReference:
         self.barrier.wait()
         times = [self.q.get(timeout=1800)[2] for _ in range(self.W)]
         solve = max(times)
-        evals = self.W * WL["samples"] * (self.L + 1)
-        per_inst = WL["samples"] * (WL["L"] + 1)
+        evals = self.W * self.wl["samples"] * (self.L + 1)
+        per_inst = self.wl["samples"] * (self.wl["L"] + 1)
         return {"inst_per_s": evals / solve / per_inst, "solve_s": solve,
                 "spread": (max(times) - min(times)) / max(times)}
 
@@ -265,11 +267,11 @@ class CpuReference:
         return {"cores": self.W, "kind": "port", "cpu_model": cpu_model(),
                 "threads": "1 BLAS/OpenMP thread per process",
                 "sample": (f"{self.W} instances in parallel (one fixed instance per process, built once; "
-                           f"workers released together by a barrier each step), {WL['samples']} samples x "
+                           f"workers released together by a barrier each step), {self.wl['samples']} samples x "
                            f"{self.L + 1} map evaluations per instance and step through oracle/sf_dense.py "
                            f"(the operation-for-operation port of the reference solve_batch, "
                            f"solver.py:286-355; the reference package itself cannot travel to the GPU box), "
-                           f"{self.warmup} warm-up + {self.steps} timed steps, extrapolated to L={WL['L']} "
+                           f"{self.warmup} warm-up + {self.steps} timed steps, extrapolated to L={self.wl['L']} "
                            f"(per-evaluation cost is constant); setup (F, F^T F, LU) excluded like the GPU plan"),
                 "median": statistics.median(v), "min": min(v), "max": max(v),
                 "setup_s_per_instance": self.setup_s}

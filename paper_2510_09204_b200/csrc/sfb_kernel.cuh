@@ -234,19 +234,33 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 // NJ: robot tile of one k-group (power of two >= n) for n <= 32; unused for n > 32 (BIG)
 // BIG2 (n = 33..64, 2D): the n > 32 kernel capped at 128 registers, 8-warp CTAs, two per SM
 // (16 warps per SM; the uncapped build needs 230 registers and runs 4-warp CTAs)
+enum { PIECE_WHOLE = 0, PIECE_HEAD = 1, PIECE_TAIL = 2 };
+// schedule slots in the misc words after the warp partials (sMisc[0..2] belong to the member solve)
+enum { SCHED_MEMBER = 3, SCHED_PIECE = 4 };
+// builds that run the split schedule: the 128-register n = 33..64 build and the 3D n <= 32
+// builds have no register to spare for it (they would spill) and always run one member per CTA
+template <int ND, bool BIG, bool BIG2>
+__host__ __device__ constexpr bool split_build() { return ND == 2 && !BIG2; }
 // One member's solve, evaluations it0 .. (max_iters or convergence), by one CTA (or one cluster).
-// hand_in >= 0: the member's state after evaluation it0 - 1 comes from the split-schedule
-// handoff slot hand_in (xi / lambda in the member's outputs); it_stop >= 0: stop before
-// evaluation it_stop and leave the state in handoff slot hand_out. Returns true when the
-// member finished (converged or reached max_iters) and its outputs are written.
+// Split schedule (sf_solve_kernel): piece = PIECE_TAIL resumes the member from the state the
+// previous CTA handed over (slot blockIdx.x - 1; xi / lambda in the member's outputs); for
+// PIECE_HEAD the loop stops before evaluation `stop` (read from shared memory each iteration,
+// so no register holds it across the solve) and hands the state to slot blockIdx.x.
+// Returns true when the member finished (converged or reached max_iters), outputs written.
 template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
-__device__ __forceinline__ bool sf_member(const KParams& P, const int b, const int it0, const int it_stop,
-                                          const int hand_in, const int hand_out) {  // @stage setup
+__device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const int piece,
+                                          const int stop) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
+  // split builds: the member's index lives in shared memory (the schedule slot the kernel
+  // writes before the solve) and is re-read where used, so the compiler need not keep it live
+  auto member = [&]() -> int {
+    if constexpr (!split_build<ND, BIG, BIG2>()) return blockIdx.x / P.csize;
+    return (int)*reinterpret_cast<const unsigned*>(smem + P.L.red + NW * 4 * 8 + SCHED_MEMBER * 4);
+  };
 
   // a member is owned by a cluster of csize CTAs; CTA rank crank owns a contiguous slice
   // of the k-group tasks and all ranks run the (identical) KKT step redundantly
@@ -257,7 +271,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
   const int nv = ND * n * NXI;       // dense outputs per member
   const int nrows = ND * n;          // (axis, robot) rows
-  const int inst = P.member_instance[b];
+  const int inst = P.member_instance[member()];
 
   double* sXi = reinterpret_cast<double*>(smem + P.L.xi);    // [ND*n][NXP]
   double* sLam = reinterpret_cast<double*>(smem + P.L.lam);  // [ND*n][NXP]
@@ -344,10 +358,10 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   {
     // a handed-over member resumes from the iterate its previous CTA left in the outputs
     // (written by another SM in this launch: read through L2)
-    const bool resume = hand_in >= 0;
-    const double* x0 = (resume ? P.xi : P.xi0) + (size_t)b * nv;
-    const double* l0 = (resume ? P.lam : P.lam0) + (size_t)b * nv;
-    const double* t0 = P.target ? P.target + (size_t)b * nv : nullptr;
+    const bool resume = piece == PIECE_TAIL;
+    const double* x0 = (resume ? P.xi : P.xi0) + (size_t)member() * nv;
+    const double* l0 = (resume ? P.lam : P.lam0) + (size_t)member() * nv;
+    const double* t0 = P.target ? P.target + (size_t)member() * nv : nullptr;
     for (int o = tid; o < nv; o += nt) {
       const int ai = o / NXI, c = o - ai * NXI;
       sXi[ai * NXP + c] = resume ? __ldcg(x0 + o) : x0[o];
@@ -415,6 +429,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   if (tid == 0) {
     sMisc[0] = 0u;
     sMisc[1] = __float_as_uint(INFINITY);
+    sMisc[2] = piece == PIECE_HEAD ? (unsigned)stop : 0xffffffffu;   // split schedule stop
   }
   __syncthreads();
   if (obs_absmax > 0.f) atomicMax(&sMisc[0], __float_as_uint(obs_absmax));
@@ -530,8 +545,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   double last_fp = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   double eq_max = 0.0, eql = 0.0;
   double fpp = 0.0;   // per-lane ||dlambda||^2 + ||dxi||^2 partial of the last KKT step
-  if (hand_in >= 0) {   // the per-thread carries of the previous CTA (same thread, same values)
-    const double* hb = P.hand + (size_t)hand_in * 2 * nt;
+  if (piece == PIECE_TAIL) {   // the per-thread carries of the previous CTA (same thread, same values)
+    const double* hb = P.hand + (size_t)(blockIdx.x - 1) * 2 * nt;
     fpp = __ldcg(hb + tid);
     eql = __ldcg(hb + nt + tid);
   }
@@ -540,17 +555,17 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   unsigned c_exact = 0, c_active = 0, c_screen = 0, c_evals = 0;
 
   for (int it = it0;; ++it) {  // @stage iter_top
-    if (it == it_stop) {
+    if (split_build<ND, BIG, BIG2>() && it == (int)sMisc[2]) {
       // split schedule: hand the state before evaluation it to the next CTA (xi / lambda
       // through the member's outputs, the per-thread carries through the handoff slot)
-      double* xo = P.xi + (size_t)b * nv;
-      double* lo = P.lam + (size_t)b * nv;
+      double* xo = P.xi + (size_t)member() * nv;
+      double* lo = P.lam + (size_t)member() * nv;
       for (int o = tid; o < nv; o += nt) {
         const int ai = o / NXI, c = o - ai * NXI;
         xo[o] = sXi[ai * NXP + c];
         lo[o] = sLam[ai * NXP + c];
       }
-      double* hb = P.hand + (size_t)hand_out * 2 * nt;
+      double* hb = P.hand + (size_t)blockIdx.x * 2 * nt;
       hb[tid] = fpp;
       hb[nt + tid] = eql;
       finished = false;
@@ -1261,7 +1276,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
     if (it > 0) last_fp = FP;
     ++c_evals;
     if (tid == 0 && crank == 0 && P.trace) {
-      double* tr = P.trace + ((size_t)b * (P.max_iters + 1) + it) * 2;
+      double* tr = P.trace + ((size_t)member() * (P.max_iters + 1) + it) * 2;
       tr[0] = primal;
       tr[1] = last_fp;
     }
@@ -1288,18 +1303,18 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
         for (int w = 0; w < NW; ++w)
           if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
       }
-      double* xo = P.xi + (size_t)b * nv;
-      double* lo = P.lam + (size_t)b * nv;
+      double* xo = P.xi + (size_t)member() * nv;
+      double* lo = P.lam + (size_t)member() * nv;
       for (int o = tid; crank == 0 && o < nv; o += nt) {
         const int ai = o / NXI, c = o - ai * NXI;
         xo[o] = sXi[ai * NXP + c];
         lo[o] = sLam[ai * NXP + c];
       }
       if (tid == 0 && crank == 0) {
-        P.primal[b] = primal;
-        P.eq_max[b] = eq_max;
-        P.iterations[b] = it;
-        P.status[b] = conv_p ? 1 : (conv_f ? 2 : 0);
+        P.primal[member()] = primal;
+        P.eq_max[member()] = eq_max;
+        P.iterations[member()] = it;
+        P.status[member()] = conv_p ? 1 : (conv_f ? 2 : 0);
       }
       break;
     }
@@ -1512,7 +1527,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
   }
 #ifdef SFB_PHASE_TIMING  // @stage epilogue
   if (tid == 0 && P.counters) {
-    for (int q = 0; q < 18; ++q) P.counters[(size_t)b * 24 + 4 + q] = (unsigned long long)t_ph[q];
+    for (int q = 0; q < 18; ++q) P.counters[(size_t)member() * 24 + 4 + q] = (unsigned long long)t_ph[q];
   }
 #endif
 
@@ -1526,9 +1541,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int b, const i
     }
     if (lane == 0) {
 #ifdef SFB_PHASE_TIMING
-      unsigned long long* cb = P.counters + (size_t)b * 24;
+      unsigned long long* cb = P.counters + (size_t)member() * 24;
 #else
-      unsigned long long* cb = P.counters + (size_t)b * 4;
+      unsigned long long* cb = P.counters + (size_t)member() * 4;
 #endif
       atomicAdd(cb + 0, w_exact);
       atomicAdd(cb + 1, w_active);
@@ -1561,40 +1576,66 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // the same code on the same state, so results are bitwise those of the unsplit launch.
   // Pieces of this CTA in order: [head of mb] [full members] [tail of ma]; one call site of
   // the (large, inlined) member solve.
-  int ma = 0, ra = 0, mb = 0, rb = 0, first = blockIdx.x / P.csize, npieces = 1;
-  const int c = blockIdx.x;
-  if (P.split) {
-    const long long E = (long long)P.max_iters + 1, U = (long long)P.B * E, G = gridDim.x;
-    const long long lo = c * U / G, hi = (c + 1) * U / G;
-    ma = (int)(lo / E); ra = (int)(lo % E); mb = (int)(hi / E); rb = (int)(hi % E);
-    first = ra ? ma + 1 : ma;
-    npieces = (rb ? 1 : 0) + (mb - first) + (ra ? 1 : 0);
+  // The piece schedule is recomputed per piece (a few integer ops) rather than kept in
+  // registers across the member solve (split_build: which builds run it; sfb_solve knows).
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* sched = reinterpret_cast<unsigned*>(smem + P.L.red + NW * 4 * 8);
+  if (!split_build<ND, BIG, BIG2>() || !P.split) {
+    if (threadIdx.x == 0) sched[SCHED_MEMBER] = blockIdx.x / P.csize;
+    __syncthreads();
+    sf_member<ND, NXI, NJ, BIG, BIG2>(P, 0, PIECE_WHOLE, 0);
+    return;
   }
-  for (int piece = 0; piece < npieces; ++piece) {
-    int b, it0 = 0, it_stop = -1, hand_in = -1, hand_out = -1;
-    if (P.split && rb && piece == 0) {            // head of mb, handed to CTA c + 1
-      b = mb;
-      it_stop = rb;
-      hand_out = c;
-    } else if (P.split && ra && piece == npieces - 1) {   // tail of ma, from CTA c - 1
-      b = ma;
-      it0 = ra;
-      hand_in = c - 1;
-      unsigned f = 0u;
-      if (threadIdx.x == 0) {
-        while ((f = ld_acquire_gpu(P.hand_flag + c - 1)) == 0u) __nanosleep(256);
+  if (threadIdx.x == 0) sched[SCHED_PIECE] = 0u;
+  __syncthreads();
+  for (;;) {
+    const int pc = (int)*reinterpret_cast<volatile unsigned*>(sched + SCHED_PIECE);
+    int b = 0, it0 = 0, piece = PIECE_WHOLE, stop = 0;
+    {
+      const long long E = (long long)P.max_iters + 1, U = (long long)P.B * E, G = gridDim.x;
+      const long long c = blockIdx.x, lo = c * U / G, hi = (c + 1) * U / G;
+      const int ma = (int)(lo / E), ra = (int)(lo % E), mb = (int)(hi / E), rb = (int)(hi % E);
+      const int first = ra ? ma + 1 : ma;
+      const int npieces = (rb ? 1 : 0) + (mb - first) + (ra ? 1 : 0);
+      if (pc >= npieces) break;
+      if (rb && pc == 0) {                        // head of mb, handed to CTA c + 1
+        b = mb;
+        piece = PIECE_HEAD;
+        stop = rb;
+      } else if (ra && pc == npieces - 1) {       // tail of ma, from CTA c - 1
+        b = ma;
+        it0 = ra;
+        piece = PIECE_TAIL;
+        unsigned f = 0u;
+        if (threadIdx.x == 0) {
+          while ((f = ld_acquire_gpu(P.hand_flag + c - 1)) == 0u) __nanosleep(256);
+        }
+        // the member may have converged inside the head: nothing left to do
+        if (__syncthreads_or(f == 2u)) {
+          if (threadIdx.x == 0) sched[SCHED_PIECE] = pc + 1;
+          __syncthreads();
+          continue;
+        }
+      } else {
+        b = first + pc - (rb ? 1 : 0);
       }
-      // the member may have converged inside the head: nothing left to do
-      if (__syncthreads_or(f == 2u)) continue;
-    } else {
-      b = first + piece - ((P.split && rb) ? 1 : 0);
     }
-    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2>(P, b, it0, it_stop, hand_in, hand_out);
+    if (threadIdx.x == 0) sched[SCHED_MEMBER] = b;
+    __syncthreads();
+    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2>(P, it0, piece, stop);
     __syncthreads();                              // shared memory reused by the next piece; handoff stores issued
-    if (hand_out >= 0 && threadIdx.x == 0) {
-      __threadfence();
-      st_release_gpu(P.hand_flag + c, fin ? 2u : 1u);
+    if (threadIdx.x == 0) {
+      const int pcn = (int)sched[SCHED_PIECE];
+      if (pcn == 0) {
+        const long long E = (long long)P.max_iters + 1, U = (long long)P.B * E;
+        if (((long long)blockIdx.x + 1) * U / gridDim.x % E != 0) {   // this was a head piece
+          __threadfence();
+          st_release_gpu(P.hand_flag + blockIdx.x, fin ? 2u : 1u);
+        }
+      }
+      sched[SCHED_PIECE] = pcn + 1;
     }
+    __syncthreads();
   }
 }
 
