@@ -35,7 +35,8 @@ namespace sfb {
 #ifndef SFB_MAXW
 #define SFB_MAXW 8
 #endif
-constexpr int NW = SFB_MAXW;     // max warps per CTA (the launch uses P.nw <= NW)
+constexpr int NW = SFB_MAXW;     // max warps per CTA of the default builds (the launch uses P.nw <= NW)
+constexpr int NW_RED = 16;       // warp-partial slots in shared memory (the widest build: 16 warps)
 constexpr int NBM = 6;           // max boundary rows per robot (rest-to-rest; 2 otherwise)
 constexpr int NT = NW * 32;      // max threads per CTA
 constexpr float PAD_SMEM = -3.0e30f;   // padded (k >= K1 or dummy body) position in shared memory
@@ -247,7 +248,7 @@ __host__ __device__ constexpr bool split_build() { return ND == 2 && !BIG2; }
 // PIECE_HEAD the loop stops before evaluation `stop` (read from shared memory each iteration,
 // so no register holds it across the solve) and hands the state to slot blockIdx.x.
 // Returns true when the member finished (converged or reached max_iters), outputs written.
-template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW>
 __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const int piece,
                                           const int stop) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
@@ -259,7 +260,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // writes before the solve) and is re-read where used, so the compiler need not keep it live
   auto member = [&]() -> int {
     if constexpr (!split_build<ND, BIG, BIG2>()) return blockIdx.x / P.csize;
-    return (int)*reinterpret_cast<const unsigned*>(smem + P.L.red + NW * 4 * 8 + SCHED_MEMBER * 4);
+    return (int)*reinterpret_cast<const unsigned*>(smem + P.L.red + NW_RED * 4 * 8 + SCHED_MEMBER * 4);
   };
 
   // a member is owned by a cluster of csize CTAs; CTA rank crank owns a contiguous slice
@@ -268,6 +269,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   const int crank = csize > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = BIG ? P.nw : NW, nt = nw * 32;   // n <= 32 always runs NW warps (compile-time strides)
+  static_assert(MW == NW || BIG2, "only the capped n > 32 build comes in a 16-warp variant");
   const int n = P.n, m = P.m, MP = P.MP, K1 = P.K1, NB = P.NB, NKG = P.NKG;
   const int nv = ND * n * NXI;       // dense outputs per member
   const int nrows = ND * n;          // (axis, robot) rows
@@ -425,7 +427,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     for (int a = 0; a < ND; ++a)
       obs_absmax = fmax_abs(obs_absmax, (float)P.obs_pos[(((size_t)inst * ND + a) * m + o) * K1 + k]);
   }
-  unsigned* sMisc = reinterpret_cast<unsigned*>(sRed + NW * 4);
+  unsigned* sMisc = reinterpret_cast<unsigned*>(sRed + NW_RED * 4);
   if (tid == 0) {
     sMisc[0] = 0u;
     sMisc[1] = __float_as_uint(INFINITY);
@@ -1222,7 +1224,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     // -------------------------------------------- D: residuals, trace, convergence  // @stage D_decision
     double S1 = 0.0, S2 = 0.0, FP = 0.0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    for (int w = 0; w < MW; ++w) {
       if (w >= nw) break;
       S1 += sRed[w * 4 + 0];
       S2 += sRed[w * 4 + 1];
@@ -1300,7 +1302,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         if (lane == 0) sRed[warp * 4 + 2] = eqp;
         __syncthreads();
         #pragma unroll
-        for (int w = 0; w < NW; ++w)
+        for (int w = 0; w < MW; ++w)
           if (w < nw) eq_max = fmax(eq_max, sRed[w * 4 + 2]);
       }
       double* xo = P.xi + (size_t)member() * nv;
@@ -1563,8 +1565,11 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false>
-__global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_kernel(const KParams P) {
+// MW = 16: the capped n > 32 build with 16-warp CTAs, one per SM (small batches and n = 65..128,
+// whose layout does not fit half an SM)
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW>
+__global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) : SFB_MINB)
+    sf_solve_kernel(const KParams P) {
   // Split schedule ("stream-K" over evaluation units): with B > G resident CTAs, one CTA per
   // member would leave the last of ceil(B / G) waves partly idle (C3: 512 members on 296
   // slots = 1.73 waves of work in 2). Instead the G CTAs form one cooperative wave and CTA c
@@ -1579,11 +1584,11 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
   // The piece schedule is recomputed per piece (a few integer ops) rather than kept in
   // registers across the member solve (split_build: which builds run it; sfb_solve knows).
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned* sched = reinterpret_cast<unsigned*>(smem + P.L.red + NW * 4 * 8);
+  unsigned* sched = reinterpret_cast<unsigned*>(smem + P.L.red + NW_RED * 4 * 8);
   if (!split_build<ND, BIG, BIG2>() || !P.split) {
     if (threadIdx.x == 0) sched[SCHED_MEMBER] = blockIdx.x / P.csize;
     __syncthreads();
-    sf_member<ND, NXI, NJ, BIG, BIG2>(P, 0, PIECE_WHOLE, 0);
+    sf_member<ND, NXI, NJ, BIG, BIG2, MW>(P, 0, PIECE_WHOLE, 0);
     return;
   }
   if (threadIdx.x == 0) sched[SCHED_PIECE] = 0u;
@@ -1622,7 +1627,7 @@ __global__ void __launch_bounds__(NT, BIG ? (BIG2 ? 2 : 1) : SFB_MINB) sf_solve_
     }
     if (threadIdx.x == 0) sched[SCHED_MEMBER] = b;
     __syncthreads();
-    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2>(P, it0, piece, stop);
+    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2, MW>(P, it0, piece, stop);
     __syncthreads();                              // shared memory reused by the next piece; handoff stores issued
     if (threadIdx.x == 0) {
       const int pcn = (int)sched[SCHED_PIECE];
