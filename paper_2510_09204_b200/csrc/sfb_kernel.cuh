@@ -700,6 +700,11 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
         };
         if constexpr (BIG) {
+          if (jc == 32) {   // full chunk: unrolled, partner rows at immediate offsets
+#pragma unroll
+            for (int j = 0; j < 32; ++j) screen(base + j * ND2);
+            return __brev(mm);
+          }
 #pragma unroll 4
           for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2);
           return __brev(mm) >> (32 - jc);
