@@ -344,6 +344,7 @@ def run_ours(args):
     systems, xi, mi = make_workload(rank)
     cfg = solver.SolverConfig(max_iters=WL["L"])
     B = xi.shape[0]
+    gidx = rank * B + np.arange(B)      # global member index of this rank's members (weak scaling)
 
     # ---- device-resident batch (kernel timing)
     batch = solver.DeviceBatch(systems, xi, None, xi, cfg=cfg, member_instance=mi, early_exit=False,
@@ -370,8 +371,8 @@ def run_ours(args):
             flush.fill_(s & 0xFF)
             starts[s].record(stream)
             batch.launch(stream)
-            if world > 1:
-                gather_results(batch, dst=0)
+            if world > 1:   # the one collective: every rank's results, trace included, to rank 0
+                gather_results(batch, dst=0, trace=True, index=gidx)
             ends[s].record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -412,28 +413,39 @@ def run_ours(args):
 
     # ---- end to end through the public serving API (host arrays in pinned memory, every
     # step packs + copies its inputs H2D and reads its whole output arena D2H; solve_stream
-    # overlaps those copies and the host packing with the neighbouring steps' kernels)
+    # overlaps those copies and the host packing with the neighbouring steps' kernels). N > 1:
+    # each rank uploads its shard, solves, the results (trace included) are gathered to rank 0
+    # over NCCL and rank 0 reads the whole job's results back.
     xi_pin = torch.from_numpy(xi).pin_memory()
     step_in = (systems, xi_pin, None, xi_pin, mi)
-    for res in solver.solve_stream(iter([step_in] * args.warmup), cfg=cfg, fixed_iterations=True,
-                                   trace=True):
-        pass
+
+    def e2e_steps(k):
+        if world == 1:
+            last = None
+            for last in solver.solve_stream(iter([step_in] * k), cfg=cfg, fixed_iterations=True,
+                                            trace=True):
+                pass
+            return (last.extra.get("h2d_bytes", 0), last.extra.get("d2h_bytes", 0)) if last else (0, 0)
+        h2d = d2h = 0
+        for _ in range(k):
+            b = solver.DeviceBatch(systems, xi_pin, None, xi_pin, cfg=cfg, member_instance=mi,
+                                   early_exit=False, trace=True)
+            b.launch()
+            flat = gather_results(b, dst=0, trace=True, index=gidx)
+            h2d = b.h2d_bytes
+            if flat is not None:
+                host = flat.cpu()
+                d2h = host.numel() * 8
+        return h2d, d2h
+
+    e2e_steps(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    n_res, gaps = 0, []
-    for res in solver.solve_stream(iter([step_in] * args.steps), cfg=cfg, fixed_iterations=True,
-                                   trace=True):
-        n_res += 1
-        gaps.append(time.perf_counter())
+    h2d, d2h = e2e_steps(args.steps)
+    torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
-    if os.environ.get("BENCH_E2E_DEBUG"):
-        print("e2e yield gaps ms", [round((b - a) * 1e3, 1) for a, b in zip([t0] + gaps, gaps)],
-              file=sys.stderr)
-    assert n_res == args.steps
-    h2d = res.extra.get("h2d_bytes", 0)
-    d2h = res.extra.get("d2h_bytes", 0)
     if world > 1:
         t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -481,10 +493,18 @@ def run_ours(args):
             "data": "synthetic (reference random_box generator + naive-prior samples)",
             "config": config_dict(world),
             "e2e": {"value": e2e_value, "unit": "instances/s", "h2d_bytes_per_step": h2d,
+                    "case": ("the reference planner's default warm start (pipeline.py:123-124): "
+                             "xi0 = target = the samples, lambda0 = 0, so the samples cross PCIe once; "
+                             "an init-net warm start would add one more xi upload"),
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps * world,
+            "comm": {"backend": backend if world > 1 else None, "world_size": world,
+                     "collective": "one gather of the final results (trace included) to rank 0 per step",
+                     "nccl_version": (".".join(map(str, torch.cuda.nccl.version()))
+                                      if world > 1 and backend == "nccl" else None)},
             "roofline": roof, "cpu_baseline": cpu, "latency": lat,
             "clocks": clk.summary(), "wall_s_timed": t_wall,
+            "step_ms": [round(v, 3) for v in ms],
             "members_per_gpu": B, "map_evaluations_per_member": WL["L"] + 1,
         }
         print(json.dumps(line), flush=True)

@@ -121,7 +121,7 @@ def gather_results(batch, dst: int = 0, B_pad: int | None = None, trace: bool = 
 
 
 def solve_sharded(systems, xi0, target=None, lam0=None, member_instance=None, kind="projection",
-                  cfg=None, fixed_iterations=False, dst=0, trace=False, group=None):
+                  cfg=None, fixed_iterations=False, dst=0, trace=False, group=None, cluster=0):
     """Each rank solves the members of its contiguous block of instances; rank `dst`
     returns the full member-major results (dict; row b = member b of the inputs, with
     "trace" (B, max_iters + 1, 2) when trace=True), other ranks None. Inputs are the
@@ -152,7 +152,7 @@ def solve_sharded(systems, xi0, target=None, lam0=None, member_instance=None, ki
                                                  if isinstance(x, torch.Tensor) else np.asarray(x)[sel])
         batch = DeviceBatch(systems[lo:hi], take(xi0), take(lam0), take(target), kind=kind, cfg=cfg,
                             member_instance=(mi[sel] - lo).astype(np.int32),
-                            early_exit=not fixed_iterations, trace=trace)
+                            early_exit=not fixed_iterations, trace=trace, cluster=cluster)
         batch.launch()
         flat = gather_results(batch, dst=dst, B_pad=B_pad, trace=trace, group=group, index=sel)
     if flat is None:

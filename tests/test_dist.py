@@ -87,7 +87,8 @@ class _FakeBatch:
 
     lo = 0
 
-    def __init__(self, systems, xi0, lam0, target, kind, cfg, member_instance, early_exit, trace):
+    def __init__(self, systems, xi0, lam0, target, kind, cfg, member_instance, early_exit, trace,
+                 cluster=0):
         mi = torch.as_tensor(np.asarray(member_instance, np.int64))
         inst = (mi + _FakeBatch.lo).to(torch.float64)
         x = torch.as_tensor(np.asarray(xi0, float))
