@@ -95,6 +95,7 @@ struct KParams {
   int split;
   unsigned* hand_flag;   // [G] 0 = pending, 1 = handed over, 2 = member already finished
   double* hand;          // [G][2 * nt] per-thread fixed-point partial and boundary-residual max
+  unsigned jitter_seed;  // race stress build only (SFB_CHECKS): 0 = no perturbation
 };
 
 // plan constant block offsets (doubles)
@@ -228,6 +229,28 @@ __host__ __device__ inline int xch_sl(int nv, int csize) { return ((xch_tot(nv) 
 #define SFB_TSUB(ph) do { } while (0)
 #endif
 
+// Race stress build (-DSFB_CHECKS, libsfb_checks.so, tools/race_stress.py): compute-sanitizer
+// is closed on this GPU pool, so the concurrency protocols (the cluster's DSMEM / mbarrier
+// exchange with parity-reused buffers, the split schedule's cross-CTA handoff, the
+// per-warp task loop against the CTA barriers) are exercised by perturbation instead: at the
+// points below a warp sleeps a pseudo-random 0..~4 us (seed KParams::jitter_seed), which
+// reorders every race window; results must stay bitwise those of the plain build, and the
+// device asserts below (trap on violation) check the protocol invariants.
+#ifdef SFB_CHECKS
+__device__ __forceinline__ void sfb_jitter(unsigned seed, unsigned site, unsigned it) {
+  if (seed == 0u) return;
+  unsigned h = seed * 0x9E3779B9u ^ (blockIdx.x * 0x85EBCA6Bu) ^ ((threadIdx.x >> 5) * 0xC2B2AE35u) ^
+               (site * 0x27D4EB2Fu) ^ (it * 0x165667B1u);
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 4) & 4095u);
+}
+#define SFB_JITTER(site, it) sfb_jitter(P.jitter_seed, (site), (unsigned)(it))
+#define SFB_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SFB_JITTER(site, it) do { } while (0)
+#define SFB_CHECK(cond) do { } while (0)
+#endif
+
 #ifndef SFB_GREG
 #define SFB_GREG 0   // n <= 32: axes of the G partials held in registers (the rest in per-lane smem slots)
 #endif
@@ -332,6 +355,14 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   };
 
   // ------------------------------------------------------------------ setup
+#ifdef SFB_CHECKS
+  {
+    unsigned dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    SFB_CHECK((unsigned)P.L.total <= dyn && (unsigned)P.L.uni + (unsigned)P.L.uni_bytes <= dyn);
+    SFB_CHECK(P.csize == 1 || (unsigned)P.L.xg + (unsigned)(P.csize * xch_sl(ND * P.n * NXI, P.csize) * 8 + 16) <= dyn);
+  }
+#endif
   for (int idx = tid; idx < w_rows(NKG) * WSTR; idx += nt) {
     const int k = idx / WSTR, c = idx - k * WSTR;
     sW[idx] = (k < K1 && c < NXI) ? P.consts[co.W + k * NXI + c] : 0.0;
@@ -590,7 +621,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     float* posw = sPos + (size_t)(warp * SUB + sub) * NJ * ND2;        // !BIG: this k-group's row
     double s1 = 0.0, s2 = 0.0;
 
+    SFB_JITTER(1, it);
     for (int ts = ts_lo + wk, tcnt = 0; ts < ts_hi; ts += nwk, ++tcnt) {
+      SFB_JITTER(2, it * 64 + ts);
       const int pslot = BIG ? 2 * wk + (tcnt & 1) : 0;
       const int kg_raw = ts * SUB + sub;
       const bool kg_ok = kg_raw < NKG;
@@ -1255,12 +1288,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #ifdef SFB_PHASE_TIMING
       if (tid == 0) t_sub = clock64();
 #endif
+      SFB_JITTER(3, it);
       for (int o = 2 * tid; o < xtot; o += 2 * nt) {
         const int sr = o / xSL;
         st_async_v2(dsmem_map(smem_u32(xrecv + (size_t)crank * xSL + (o - sr * xSL)), sr), sG[o], sG[o + 1],
                     dsmem_map(xbar1, sr));
       }
+      SFB_JITTER(4, it);
       mbar_wait(xbar1, par);
+      SFB_JITTER(5, it);
       SFB_TSUB(11);
       if (tid == 0) mbar_expect_tx(xbar2, (uint32_t)(xtot * 8));
       const int mylen = slice_len(crank);
@@ -1273,6 +1309,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         const uint32_t dst = smem_u32(sG + crank * xSL + j);
         for (int r = 0; r < csize; ++r) st_async_v2(dsmem_map(dst, r), a0, a1, dsmem_map(xbar2, r));
       }
+      SFB_JITTER(6, it);
       mbar_wait(xbar2, par);
       SFB_TSUB(12);
       S1 = sG[nv];
@@ -1530,6 +1567,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       }
     }
     __syncthreads();
+    SFB_JITTER(7, it);
     SFB_TMARK(5);
   }
 #ifdef SFB_PHASE_TIMING  // @stage epilogue
@@ -1619,6 +1657,7 @@ __global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) 
         unsigned f = 0u;
         if (threadIdx.x == 0) {
           while ((f = ld_acquire_gpu(P.hand_flag + c - 1)) == 0u) __nanosleep(256);
+          SFB_CHECK(f == 1u || f == 2u);
         }
         // the member may have converged inside the head: nothing left to do
         if (__syncthreads_or(f == 2u)) {
@@ -1639,7 +1678,9 @@ __global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) 
       if (pcn == 0) {
         const long long E = (long long)P.max_iters + 1, U = (long long)P.B * E;
         if (((long long)blockIdx.x + 1) * U / gridDim.x % E != 0) {   // this was a head piece
+          SFB_JITTER(8, pcn);
           __threadfence();
+          SFB_CHECK(ld_acquire_gpu(P.hand_flag + blockIdx.x) == 0u);   // each slot handed over once
           st_release_gpu(P.hand_flag + blockIdx.x, fin ? 2u : 1u);
         }
       }
