@@ -626,7 +626,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       SFB_JITTER(2, it * 64 + ts);
       const int pslot = BIG ? 2 * wk + (tcnt & 1) : 0;
       const int kg_raw = ts * SUB + sub;
-      const bool kg_ok = kg_raw < NKG;
+      const bool kg_ok = (!BIG && SUB == 1) || kg_raw < NKG;   // TBL: one k-group per task, ts < NTS = NKG
       const int kg = kg_ok ? kg_raw : NKG - 1;
       const bool live = robot_ok && kg_ok;
       const bool has1 = 2 * kg + 1 < K1;
