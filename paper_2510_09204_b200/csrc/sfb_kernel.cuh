@@ -402,6 +402,11 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       sTgt[o] = t0 ? t0[o] : 0.0;
     }
   }
+  // xi's padding columns feed the positions' DMMA (times a zero W column): keep them zero
+  for (int idx = tid; idx < ND * n * (NXP - NXI); idx += nt) {
+    const int r = idx / (NXP - NXI);
+    sXi[r * NXP + NXI + (idx - r * (NXP - NXI))] = 0.0;
+  }
   // obstacles, padded to MP (multiple of 4) with far-away dummies that never screen in
   for (int o = tid; o < MP; o += nt) {
     float* st = sObsS + o * OS;
@@ -604,6 +609,52 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       finished = false;
       break;
     }
+    // -------------------------------------------- A (TBL): positions of every step on DMMA  // @stage A_positions
+    // P (k x col) = W (k x c) . X^T (c x col), X[col][c] = xi of the (axis, robot) row col, into
+    // the g table (sTab[k][col ^ tab_swz(k)]): warp per 8 x 8 tile, k-dim c in steps of 4. A
+    // task reads its own and its partners' positions from there and overwrites its rows with
+    // g_i(k) once its rows are done (no other task reads them). Rows outside this CTA's steps
+    // [klo, khi) are not stored (the contraction masks them).
+    if (TBL) {
+      const int ncol = ND * n, ntn = (ncol + 7) >> 3;
+      const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
+      const int mt0 = klo >> 3, ntm = ((khi + 7) >> 3) - mt0;
+      const int rq = lane >> 2, kq = lane & 3;
+      constexpr int NKS = (NXI + 3) / 4;
+      // A warp owns a column tile (its B fragments loaded once) and every G-th row tile of
+      // it (G row groups per column tile so that every warp has work). No operand masks: W is
+      // zero for c >= NXI and xi's padding columns are zero (set up once, never written), or
+      // (NXP < 4 NKS) the next row's finite value times that zero; rows past K1 and columns
+      // past ND n read finite neighbouring buffers and are never stored.
+      const int G = (nw + ntn - 1) / ntn;
+      const int swl = (rq & 3) << 2;                 // tab_swz of every row this lane stores
+      for (int item = warp; item < ntn * G; item += nw) {
+        const int rg = item / ntn, nt2 = item - rg * ntn;
+        const int colb = nt2 * 8 + rq, col = nt2 * 8 + 2 * kq;
+        double bfr[NKS];
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+          const int c = 4 * ks + kq;
+          bfr[ks] = (4 * NKS > NXP && c >= NXI) ? 0.0 : sXi[colb * NXP + c];   // crossed into the next row
+        }
+        const bool pair_ok = col + 1 < ncol, one_ok = col < ncol;
+        const double* wa = sW + ((mt0 + rg) * 8 + rq) * WSTR + kq;
+        double* dst = sTab + ((mt0 + rg) * 8 + rq) * TS + (col ^ swl);
+        int kr = (mt0 + rg) * 8 + rq;
+        for (int mt = rg; mt < ntm; mt += G, wa += 8 * G * WSTR, dst += 8 * G * TS, kr += 8 * G) {
+          double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < NKS; ++ks)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc0), "+d"(acc1) : "d"(wa[4 * ks]), "d"(bfr[ks]));
+          if (kr >= klo && kr < khi) {
+            if (pair_ok) *reinterpret_cast<double2*>(dst) = make_double2(acc0, acc1);
+            else if (one_ok) *dst = acc0;
+          }
+        }
+      }
+      __syncthreads();
+    }
     // -------------------------------------------- A/B/C per k-group task
     // G partials (not TBL): the first RA axes in registers, the rest in per-lane smem slots
     constexpr int RA = BIG ? ND : (SFB_GREG > ND ? ND : SFB_GREG);
@@ -637,11 +688,24 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #endif
 
       // A: exact positions of the lane's robot at the two steps  // @stage A_positions
+      // (TBL: from the table phase A filled; a missing second step or an idle lane reads a
+      // valid cell of the task's first step)
+      const int k0 = 2 * kg, k1 = has1 ? k0 + 1 : k0;
+      const double* tr0 = sTab + (size_t)k0 * TS;
+      const double* tr1 = sTab + (size_t)k1 * TS;
+      const int sw0 = tab_swz(k0), sw1 = tab_swz(k1);
       double p[ND][2];
 #pragma unroll
-      for (int a = 0; a < ND; ++a) p[a][0] = p[a][1] = 0.0;
+      for (int a = 0; a < ND; ++a) {
+        if (TBL) {
+          p[a][0] = tr0[(a * n + ic) ^ sw0];
+          p[a][1] = tr1[(a * n + ic) ^ sw1];
+        } else {
+          p[a][0] = p[a][1] = 0.0;
+        }
+      }
 #pragma unroll
-      for (int c = 0; c + 1 < NXI; c += 2) {
+      for (int c = 0; !TBL && c + 1 < NXI; c += 2) {
         const double2 u0 = *reinterpret_cast<const double2*>(w0r + c);
         const double2 u1 = *reinterpret_cast<const double2*>(w1r + c);
 #pragma unroll
@@ -651,7 +715,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           p[a][1] = fma(u1.y, x.y, fma(u1.x, x.x, p[a][1]));
         }
       }
-      if (NXI & 1) {
+      if (!TBL && (NXI & 1)) {
         const double u0 = w0r[NXI - 1], u1 = w1r[NXI - 1];
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
@@ -748,7 +812,95 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         }
       };
 
-      {
+      // obstacle screen of the chunk o0 .. o0 + 31: bit o set if obstacle o0 + o may be within
+      // contact at one of the lane's steps (always 0 past MP or for an idle lane)
+      auto obs_screen = [&](const int o0) -> unsigned {  // @stage B_obs_screen
+        if (o0 >= MP) return 0u;
+        const int oc = min(32, MP - o0);
+        unsigned mask = 0u;
+        if (!force) {
+          unsigned mm = 0u;
+          if (compact) {
+            // grid candidates of the lane's two positions, each confirmed by the FP32 test
+            // (per lane: a robot is near few obstacles)
+            auto cell = [&](float x, float y) -> unsigned {
+              const int cx = __float2int_rd((x - sKF[KC_F_GX0]) * sKF[KC_F_GIX]);
+              const int cy = __float2int_rd((y - sKF[KC_F_GY0]) * sKF[KC_F_GIY]);
+              return ((unsigned)cx < (unsigned)GRID && (unsigned)cy < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
+            };
+            unsigned cand = live ? cell(own[0][0], own[1][0]) : 0u;
+            if (live && has1) cand |= cell(own[0][1], own[1][1]);
+            while (cand) {
+              const int o = __ffs(cand) - 1;
+              cand &= cand - 1u;
+              const float4 v = *reinterpret_cast<const float4*>(sObsS + o * OS);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
+              const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
+              float2 q;
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(sObsS + o * OS + 4);
+                const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
+                                             make_float2(own[ND - 1][0], own[ND - 1][1]));
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
+                q = __ffma2_rn(dy, dy, q);
+              } else {
+                q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
+              }
+              q = __ffma2_rn(dx, dx, q);
+              if ((int)(__float_as_uint(q.x) | __float_as_uint(q.y)) < 0) mm |= 1u << o;
+            }
+            mm = __brev(mm << (32 - oc));   // undone by the shared bit reversal below
+          } else if (P.obs_static) {
+            // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
+            const float* ob = sObsS + (size_t)o0 * OS;
+            for (int o4 = 0; o4 < oc; o4 += 4)   // MP is a multiple of 4
+#pragma unroll
+            for (int o = o4; o < o4 + 4; ++o) {
+              const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
+              const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
+              float2 q;
+              if (ND == 3) {
+                const float4 v2 = *reinterpret_cast<const float4*>(ob + o * OS + 4);
+                const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
+                                             make_float2(own[ND - 1][0], own[ND - 1][1]));
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
+                q = __ffma2_rn(dy, dy, q);
+              } else {
+                q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
+              }
+              q = __ffma2_rn(dx, dx, q);
+              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+            }
+          } else {
+            const float* obase = sObs + ((size_t)kg * MP + o0) * ND2;
+#pragma unroll 4
+            for (int o = 0; o < oc; ++o) {
+              const float4 v = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2);
+              const float th = sObsThr[o0 + o];
+              const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
+              const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
+              float2 q = __ffma2_rn(dy, dy, make_float2(-th, -th));
+              q = __ffma2_rn(dx, dx, q);
+              if (ND == 3) {
+                const float kp = sObsThr[MP + o0 + o];
+                const float4 v2 = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2 + 4);
+                const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
+                q = __ffma2_rn(__fmul2_rn(dz, make_float2(kp, kp)), dz, q);
+              }
+              mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
+            }
+          }
+          mask = __brev(mm) >> (32 - oc);
+        } else {
+          const int ov = max(0, min(32, m - o0));
+          mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
+        }
+        if (!live) mask = 0u;
+        return mask;
+      };
+
+      {  // @stage B_pair_exact
         // n <= 32 with static obstacles (one chunk): the exact pair and obstacle rows run in one
         // loop, a lane's pair bits first then its obstacle bits — each lane's order of the
         // two-loop form, in max(pairs + obstacles) instead of max(pairs) + max(obstacles) steps
@@ -827,87 +979,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #else
         for (int o0 = 0; o0 < MP; o0 += 32) {
 #endif
-          const int oc = min(32, MP - o0);
-          unsigned mask = 0u;
-          if (!force) {
-            unsigned mm = 0u;
-            if (compact) {
-              // grid candidates of the lane's two positions, each confirmed by the FP32 test
-              // (per lane: a robot is near few obstacles)
-              auto cell = [&](float x, float y) -> unsigned {
-                const int cx = __float2int_rd((x - sKF[KC_F_GX0]) * sKF[KC_F_GIX]);
-                const int cy = __float2int_rd((y - sKF[KC_F_GY0]) * sKF[KC_F_GIY]);
-                return ((unsigned)cx < (unsigned)GRID && (unsigned)cy < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
-              };
-              unsigned cand = live ? cell(own[0][0], own[1][0]) : 0u;
-              if (live && has1) cand |= cell(own[0][1], own[1][1]);
-              while (cand) {
-                const int o = __ffs(cand) - 1;
-                cand &= cand - 1u;
-                const float4 v = *reinterpret_cast<const float4*>(sObsS + o * OS);
-                const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
-                const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
-                float2 q;
-                if (ND == 3) {
-                  const float4 v2 = *reinterpret_cast<const float4*>(sObsS + o * OS + 4);
-                  const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
-                                               make_float2(own[ND - 1][0], own[ND - 1][1]));
-                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
-                  q = __ffma2_rn(dy, dy, q);
-                } else {
-                  q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
-                }
-                q = __ffma2_rn(dx, dx, q);
-                if ((int)(__float_as_uint(q.x) | __float_as_uint(q.y)) < 0) mm |= 1u << o;
-              }
-              mm = __brev(mm << (32 - oc));   // undone by the shared bit reversal below
-            } else if (P.obs_static) {
-              // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
-              const float* ob = sObsS + (size_t)o0 * OS;
-              for (int o4 = 0; o4 < oc; o4 += 4)   // MP is a multiple of 4
-#pragma unroll
-              for (int o = o4; o < o4 + 4; ++o) {
-                const float4 v = *reinterpret_cast<const float4*>(ob + o * OS);
-                const float2 dx = __fadd2_rn(make_float2(v.x, v.x), make_float2(own[0][0], own[0][1]));
-                const float2 dy = __fadd2_rn(make_float2(v.y, v.y), make_float2(own[1][0], own[1][1]));
-                float2 q;
-                if (ND == 3) {
-                  const float4 v2 = *reinterpret_cast<const float4*>(ob + o * OS + 4);
-                  const float2 dz = __fadd2_rn(make_float2(v.z, v.z),
-                                               make_float2(own[ND - 1][0], own[ND - 1][1]));
-                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(v2.x, v2.x)), dz, make_float2(v.w, v.w));
-                  q = __ffma2_rn(dy, dy, q);
-                } else {
-                  q = __ffma2_rn(dy, dy, make_float2(v.z, v.z));
-                }
-                q = __ffma2_rn(dx, dx, q);
-                mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
-              }
-            } else {
-              const float* obase = sObs + ((size_t)kg * MP + o0) * ND2;
-#pragma unroll 4
-              for (int o = 0; o < oc; ++o) {
-                const float4 v = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2);
-                const float th = sObsThr[o0 + o];
-                const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
-                const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
-                float2 q = __ffma2_rn(dy, dy, make_float2(-th, -th));
-                q = __ffma2_rn(dx, dx, q);
-                if (ND == 3) {
-                  const float kp = sObsThr[MP + o0 + o];
-                  const float4 v2 = *reinterpret_cast<const float4*>(obase + (size_t)o * ND2 + 4);
-                  const float2 dz = __fadd2_rn(make_float2(v2.x, v2.y), nz);
-                  q = __ffma2_rn(__fmul2_rn(dz, make_float2(kp, kp)), dz, q);
-                }
-                mm = push_hit(mm, __float_as_uint(q.x) | __float_as_uint(q.y));
-              }
-            }
-            mask = __brev(mm) >> (32 - oc);
-          } else {
-            const int ov = max(0, min(32, m - o0));
-            mask = (ov >= 32) ? FULL : ((1u << ov) - 1u);
-          }
-          if (!live) mask = 0u;
+          unsigned mask = obs_screen(o0);
 #ifdef SFB_EXP_NOEXACT
           if (__float_as_uint(own[0][0]) != 0x12345678u) mask = 0u;
 #endif
@@ -948,8 +1020,11 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
             // apart from the row math's rare slow path (partner position and row parameters
             // by select), so a pass costs the same for pair and obstacle rows
             unsigned pmk = pdef, omk = mask;
-            const double pia2 = sKD[KC_INV_A2], pib2 = sKD[KC_INV_B2], pa = sKD[KC_RA], pb = sKD[KC_RB];
-            while (__any_sync(FULL, (pmk | omk) != 0u)) {
+            const int tb0 = P.L.gl / 8 + k0 * TS, tb1 = P.L.gl / 8 + k1 * TS, ob0 = P.L.obs_c / 8;
+            // TBL: a partner robot's exact positions come from the table (phase A), so each
+            // lane runs its own rows without warp-synchronous exchanges; obstacle centres and
+            // axes from shared memory (the pair axes are the double4 at sKD[KC_INV_A2])
+            while (TBL ? ((pmk | omk) != 0u) : __any_sync(FULL, (pmk | omk) != 0u)) {
               const bool isp = pmk != 0u;
               const bool act = isp || omk != 0u;
               const int bit = __ffs(isp ? pmk : omk) - 1;          // -1: no row left
@@ -957,22 +1032,33 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
               omk = isp ? omk : (omk & (omk - 1u));
               const int jl = isp ? bit : 0, o = isp ? 0 : max(bit, 0);
               double pj[ND][2];
-              if (__any_sync(FULL, isp)) {
-                const int src = sub * LW + jl;
+              if (TBL) {
+                // 32-bit shared-memory offsets (in doubles) selected per row kind
+                const double* sb = reinterpret_cast<const double*>(smem);
 #pragma unroll
-                for (int a = 0; a < ND; ++a)
+                for (int a = 0; a < ND; ++a) {
+                  const int q0 = isp ? tb0 + ((a * n + jl) ^ sw0) : ob0 + o * ND + a;
+                  const int q1 = isp ? tb1 + ((a * n + jl) ^ sw1) : q0;
+                  pj[a][0] = sb[q0];
+                  pj[a][1] = sb[q1];
+                }
+              } else {
+                if (__any_sync(FULL, isp)) {
+                  const int src = sub * LW + jl;
 #pragma unroll
-                  for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+                  for (int a = 0; a < ND; ++a)
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) pj[a][kk] = __shfl_sync(FULL, p[a][kk], src);
+                }
+                if (!isp) {
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
+                }
               }
-              const double4 ax = *reinterpret_cast<const double4*>(sObsAx + 4 * o);
-              if (!isp) {
-#pragma unroll
-                for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
-              }
-              const double ia2 = isp ? pia2 : ax.x, ib2 = isp ? pib2 : ax.y;
-              const double aa = isp ? pa : ax.z, bb = isp ? pb : ax.w;
-              const double cs = (!isp || i < jl) ? 1.0 : -1.0;
+              const double4 ax = *reinterpret_cast<const double4*>(smem + (isp ? P.L.kc + KC_INV_A2 * 8 : P.L.obs_ax + 32 * o));
+              const double ia2 = ax.x, ib2 = ax.y, aa = ax.z, bb = ax.w;
               const bool once = !isp || i < jl;   // rows the reference's F holds once
+              const double cs = once ? 1.0 : -1.0;
 #pragma unroll
               for (int kk = 0; kk < 2; ++kk) {
                 if (act && kk < nsteps) {
@@ -1010,13 +1096,16 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       // all strictly inside skips the rows, which are then exactly zero.
       bool box_rows = true;
       if (compact && !force) {
+        // per axis: the larger / smaller of the lane's steps against the shrunk box (a missing
+        // second step repeats the first; a lane without steps is never out). NaN positions
+        // need no rows here: the FP64 rows below add nothing for them either.
         bool out = false;
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-#pragma unroll
-          for (int a = 0; a < ND; ++a)
-            if (kk < nsteps) out |= !(own[a][kk] <= sKF[KC_F_BHI + a] && own[a][kk] >= sKF[KC_F_BLO + a]);
-        box_rows = __any_sync(FULL, out);
+        for (int a = 0; a < ND; ++a) {
+          const float v1 = has1 ? own[a][1] : own[a][0];
+          out |= (fmaxf(own[a][0], v1) > sKF[KC_F_BHI + a]) | (fminf(own[a][0], v1) < sKF[KC_F_BLO + a]);
+        }
+        box_rows = __any_sync(FULL, live && out);
       }  // @stage box
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
@@ -1034,15 +1123,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       // C: TBL stores g_i(k) for the tensor-core contraction after the task loop; otherwise
       // contraction with W^T into the lane's partial G  // @stage C_contract
       if (TBL) {
+        __syncwarp();   // every lane's rows have read the partner positions of these steps
         if (live) {
+          double* w0 = const_cast<double*>(tr0);
+          double* w1 = const_cast<double*>(tr1);
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            if (kk < nsteps)
-#pragma unroll
-              for (int a = 0; a < ND; ++a) {
-                const int k = 2 * kg + kk;
-                sTab[(size_t)k * TS + ((a * n + i) ^ tab_swz(k))] = g[a][kk];
-              }
+          for (int a = 0; a < ND; ++a) {
+            w0[(a * n + i) ^ sw0] = g[a][0];
+            if (has1) w1[(a * n + i) ^ sw1] = g[a][1];
+          }
         }
       } else if (__any_sync(FULL, nsteps > 0)) {
 #pragma unroll
