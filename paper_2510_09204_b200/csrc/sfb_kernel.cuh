@@ -131,15 +131,35 @@ constexpr int WSTR = 12;
 __host__ __device__ constexpr int w_rows(int nkg) { return (2 * nkg + 3) & ~3; }
 
 __device__ __forceinline__ float fmax_abs(float a, float b) { return fmaxf(a, fabsf(b)); }
+// a value the compiler must keep in a register (it cannot rematerialize an asm result): used for
+// per-task flags that register pressure would otherwise make it recompute at every use
+__device__ __forceinline__ int opaque(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// shared-memory loads at a 32-bit shared-window address (no generic-address arithmetic)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
 
 // append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
 __device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __funnelshift_l(t, m, 1); }
 
 // 1/sqrt(q) in FP64 from the FP32 MUFU seed and one Newton step (relative error ~1e-14,  // @stage exact_math
 // vs ~1e-16 for rsqrt(double); the seed needs q inside the FP32 normal range)
-__device__ __forceinline__ double rsqrt_fast01(double q) {
-  if (!(q > 1e-30)) return rsqrt(q);
-  const double y = (double)rsqrtf((float)q);
+__device__ __forceinline__ double rsqrt_fast01(double q) {   // 1e-30 < q < 1
+  float ys;   // (float)q is a normal number here: the flush-to-zero MUFU form needs no range fix-up
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ys) : "f"((float)q));
+  const double y = (double)ys;
   return y * fma(-0.5 * q, y * y, 1.5);
 }
 
@@ -153,14 +173,16 @@ __device__ __forceinline__ bool row_exact(const double (&d)[ND], double inv_a2, 
   double q = (d[0] * d[0] + d[1] * d[1]) * inv_a2;
   if (ND == 3) q = fma(d[ND - 1] * d[ND - 1], inv_b2, q);
   double f;
-  if (q < 1.0) {
+  if (q < 1.0 && q > 1e-30) {        // the active rows: 1 - 1/rho from the FP32 seed + Newton
+    f = 1.0 - rsqrt_fast01(q);
+  } else if (q < 1.0) {              // rho ~ 0: coincident rows, or an exact rsqrt
     if (q == 0.0) {
       r[0] = -ax_a * coinc_sign;
       r[1] = 0.0 * coinc_sign;
       if (ND == 3) r[ND - 1] = -ax_b * COS_HALF_PI * coinc_sign;
       return true;
     }
-    f = 1.0 - rsqrt_fast01(q);
+    f = 1.0 - rsqrt(q);
   } else if (q > d_max * d_max) {
     f = 1.0 - d_max * rsqrt(q);
   } else {
@@ -570,7 +592,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     rbk = 0; wk = warp; nwk = nw;
   }
   const int i = BIG ? rbk * 32 + lane : lane % LW;
-  const bool robot_ok = i < n;
+  const bool robot_ok = opaque(i < n ? 1 : 0) != 0;
   const int ic = robot_ok ? i : n - 1;
   const int NTS = (NKG + SUB - 1) / SUB;
   const int ts_lo = (NTS * crank) / csize, ts_hi = (NTS * (crank + 1)) / csize;
@@ -680,7 +702,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       const bool kg_ok = (!BIG && SUB == 1) || kg_raw < NKG;   // TBL: one k-group per task, ts < NTS = NKG
       const int kg = kg_ok ? kg_raw : NKG - 1;
       const bool live = robot_ok && kg_ok;
-      const bool has1 = 2 * kg + 1 < K1;
+      const bool has1 = opaque(2 * kg + 1 < K1 ? 1 : 0) != 0;
       const double* w0r = sW + (size_t)(2 * kg) * WSTR;   // W rows of the two steps
       const double* w1r = w0r + WSTR;
 #ifdef SFB_PHASE_TIMING
@@ -783,7 +805,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         const float2 thr2 = make_float2(-r_thr, -r_thr);
         const float* base = BIG ? sPos + ((size_t)pslot * NROW + j0) * ND2 : posw;
         unsigned mm = 0u;
-        auto screen = [&](const float* bp) {
+        auto screen = [&](const float* bp, unsigned& mm) {
           const float4 v = *reinterpret_cast<const float4*>(bp);
           const float2 dx = __fadd2_rn(make_float2(v.x, v.y), nx);
           const float2 dy = __fadd2_rn(make_float2(v.z, v.w), ny);
@@ -799,15 +821,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         if constexpr (BIG) {
           if (jc == 32) {   // full chunk: unrolled, partner rows at immediate offsets
 #pragma unroll
-            for (int j = 0; j < 32; ++j) screen(base + j * ND2);
+            for (int j = 0; j < 32; ++j) screen(base + j * ND2, mm);
             return __brev(mm);
           }
 #pragma unroll 4
-          for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2);
+          for (int j = 0; j < jc; ++j) screen(base + (size_t)j * ND2, mm);
           return __brev(mm) >> (32 - jc);
         } else {
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) screen(base + j * ND2);
+          for (int j = 0; j < NJ; ++j) screen(base + j * ND2, mm);
           return (__brev(mm) >> (32 - NJ)) & ((jc >= 32) ? FULL : ((1u << jc) - 1u));
         }
       };
@@ -1021,6 +1043,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
             // by select), so a pass costs the same for pair and obstacle rows
             unsigned pmk = pdef, omk = mask;
             const int tb0 = P.L.gl / 8 + k0 * TS, tb1 = P.L.gl / 8 + k1 * TS, ob0 = P.L.obs_c / 8;
+            const uint32_t sbase = smem_u32(smem);
             // TBL: a partner robot's exact positions come from the table (phase A), so each
             // lane runs its own rows without warp-synchronous exchanges; obstacle centres and
             // axes from shared memory (the pair axes are the double4 at sKD[KC_INV_A2])
@@ -1033,14 +1056,13 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
               const int jl = isp ? bit : 0, o = isp ? 0 : max(bit, 0);
               double pj[ND][2];
               if (TBL) {
-                // 32-bit shared-memory offsets (in doubles) selected per row kind
-                const double* sb = reinterpret_cast<const double*>(smem);
+                // 32-bit shared-window addresses selected per row kind
 #pragma unroll
                 for (int a = 0; a < ND; ++a) {
                   const int q0 = isp ? tb0 + ((a * n + jl) ^ sw0) : ob0 + o * ND + a;
                   const int q1 = isp ? tb1 + ((a * n + jl) ^ sw1) : q0;
-                  pj[a][0] = sb[q0];
-                  pj[a][1] = sb[q1];
+                  pj[a][0] = lds_f64(sbase + 8 * q0);
+                  pj[a][1] = lds_f64(sbase + 8 * q1);
                 }
               } else {
                 if (__any_sync(FULL, isp)) {
@@ -1055,8 +1077,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                   for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
                 }
               }
-              const double4 ax = *reinterpret_cast<const double4*>(smem + (isp ? P.L.kc + KC_INV_A2 * 8 : P.L.obs_ax + 32 * o));
-              const double ia2 = ax.x, ib2 = ax.y, aa = ax.z, bb = ax.w;
+              double ia2, ib2, aa, bb;
+              if (TBL) {
+                const uint32_t axa = sbase + (isp ? P.L.kc + KC_INV_A2 * 8 : P.L.obs_ax + 32 * o);
+                const double2 a01 = lds_f64x2(axa), a23 = lds_f64x2(axa + 16);
+                ia2 = a01.x; ib2 = a01.y; aa = a23.x; bb = a23.y;
+              } else {
+                const double4 ax = *reinterpret_cast<const double4*>(isp ? sKD + KC_INV_A2 : sObsAx + 4 * o);
+                ia2 = ax.x; ib2 = ax.y; aa = ax.z; bb = ax.w;
+              }
               const bool once = !isp || i < jl;   // rows the reference's F holds once
               const double cs = once ? 1.0 : -1.0;
 #pragma unroll
