@@ -138,6 +138,10 @@ __device__ __forceinline__ int opaque(int v) {
   asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
 }
+// ... only where registers allow it (otherwise the value itself: the builds at the register cap
+// would spill the extra live registers)
+template <bool ON>
+__device__ __forceinline__ int keep(int v) { return ON ? opaque(v) : v; }
 
 // shared-memory loads at a 32-bit shared-window address (no generic-address arithmetic)
 __device__ __forceinline__ double lds_f64(uint32_t a) {
@@ -298,6 +302,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                                           const int stop) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
   constexpr int NXP = nxi_pad(NXI);        // padded coefficient stride in shared memory
+  constexpr bool KEEP = !BIG && ND == 2;   // per-task flags pinned in registers (see keep())
   constexpr int OS = (ND == 2) ? 4 : 8;    // floats per static obstacle
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -503,7 +508,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // 1.001 a_o + 1e-6 around the centre: every row the FP32 screen could flag (|p - c| < a
   // sqrt(1 + 2e-3) with FP32 positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a,
   // so no active row is lost; candidates are then confirmed by the screen's own FP32 test.
-  const bool compact = !BIG && P.compact && (m == 0 || P.obs_static);
+  const bool compact = !BIG && keep<KEEP>(P.compact && (m == 0 || P.obs_static) ? 1 : 0) != 0;
   unsigned* sGrid = reinterpret_cast<unsigned*>(smem + P.L.grid);
   double* sKD = reinterpret_cast<double*>(smem + P.L.kc);
   float* sKF = reinterpret_cast<float*>(sKD + KC_NDBL);
@@ -518,8 +523,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     }
     const double hx = (x1 - x0) / GRID, hy = (y1 - y0) / GRID;
     if (tid == 0) {
-      sKF[KC_F_GX0] = (float)x0;
-      sKF[KC_F_GY0] = (float)y0;
+      // cell coordinate u = (x - x0) / hx as one FMA: x * (1 / hx) + (-x0 / hx)
+      sKF[KC_F_GX0] = (float)(-x0 / hx);
+      sKF[KC_F_GY0] = (float)(-y0 / hy);
       sKF[KC_F_GIX] = (float)(1.0 / hx);
       sKF[KC_F_GIY] = (float)(1.0 / hy);
     }
@@ -592,8 +598,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     rbk = 0; wk = warp; nwk = nw;
   }
   const int i = BIG ? rbk * 32 + lane : lane % LW;
-  const bool robot_ok = opaque(i < n ? 1 : 0) != 0;
-  const int ic = robot_ok ? i : n - 1;
+  const bool robot_ok = keep<KEEP>(i < n ? 1 : 0) != 0;
+  const int ic = keep<KEEP>(robot_ok ? i : n - 1);
   const int NTS = (NKG + SUB - 1) / SUB;
   const int ts_lo = (NTS * crank) / csize, ts_hi = (NTS * (crank + 1)) / csize;
   const double* xrow = sXi + (size_t)ic * NXP;   // axis a at + a * n * NXP
@@ -702,7 +708,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       const bool kg_ok = (!BIG && SUB == 1) || kg_raw < NKG;   // TBL: one k-group per task, ts < NTS = NKG
       const int kg = kg_ok ? kg_raw : NKG - 1;
       const bool live = robot_ok && kg_ok;
-      const bool has1 = opaque(2 * kg + 1 < K1 ? 1 : 0) != 0;
+      const bool has1 = keep<KEEP>(2 * kg + 1 < K1 ? 1 : 0) != 0;
       const double* w0r = sW + (size_t)(2 * kg) * WSTR;   // W rows of the two steps
       const double* w1r = w0r + WSTR;
 #ifdef SFB_PHASE_TIMING
@@ -845,13 +851,16 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           if (compact) {
             // grid candidates of the lane's two positions, each confirmed by the FP32 test
             // (per lane: a robot is near few obstacles)
-            auto cell = [&](float x, float y) -> unsigned {
-              const int cx = __float2int_rd((x - sKF[KC_F_GX0]) * sKF[KC_F_GIX]);
-              const int cy = __float2int_rd((y - sKF[KC_F_GY0]) * sKF[KC_F_GIY]);
-              return ((unsigned)cx < (unsigned)GRID && (unsigned)cy < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
+            // (the FMA's rounding moves u by ~1e-5 of a cell, well inside the cells' 1e-3 widening)
+            const float4 gk = *reinterpret_cast<const float4*>(sKF + KC_F_GX0);   // bx by ax ay
+            const float2 ux = __ffma2_rn(make_float2(own[0][0], own[0][1]), make_float2(gk.z, gk.z), make_float2(gk.x, gk.x));
+            const float2 uy = __ffma2_rn(make_float2(own[1][0], own[1][1]), make_float2(gk.w, gk.w), make_float2(gk.y, gk.y));
+            auto cell = [&](float u, float v) -> unsigned {
+              const int cx = __float2int_rd(u), cy = __float2int_rd(v);
+              return ((unsigned)(cx | cy) < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
             };
-            unsigned cand = live ? cell(own[0][0], own[1][0]) : 0u;
-            if (live && has1) cand |= cell(own[0][1], own[1][1]);
+            unsigned cand = live ? cell(ux.x, uy.x) : 0u;
+            if (live && has1) cand |= cell(ux.y, uy.y);
             while (cand) {
               const int o = __ffs(cand) - 1;
               cand &= cand - 1u;
