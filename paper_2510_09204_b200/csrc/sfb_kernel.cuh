@@ -508,7 +508,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // 1.001 a_o + 1e-6 around the centre: every row the FP32 screen could flag (|p - c| < a
   // sqrt(1 + 2e-3) with FP32 positions) lies in such a cell, and in 3D rho >= |(dx, dy)| / a,
   // so no active row is lost; candidates are then confirmed by the screen's own FP32 test.
-  const bool compact = !BIG && keep<KEEP>(P.compact && (m == 0 || P.obs_static) ? 1 : 0) != 0;
+  const bool compact = keep<KEEP>(P.compact && (m == 0 || P.obs_static) ? 1 : 0) != 0;
   unsigned* sGrid = reinterpret_cast<unsigned*>(smem + P.L.grid);
   double* sKD = reinterpret_cast<double*>(smem + P.L.kc);
   float* sKF = reinterpret_cast<float*>(sKD + KC_NDBL);
