@@ -935,8 +935,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         // n <= 32 with static obstacles (one chunk): the exact pair and obstacle rows run in one
         // loop, a lane's pair bits first then its obstacle bits — each lane's order of the
         // two-loop form, in max(pairs + obstacles) instead of max(pairs) + max(obstacles) steps
-        const bool merge = !BIG && P.obs_static && m > 0 && MP <= 32;
+        const bool merge = P.obs_static && m > 0 && MP <= 32;
         unsigned pdef = 0u;
+        int pj0 = 0;   // first robot of the pair chunk deferred to the merged loop
         // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
         for (int j0 = 0; j0 < (BIG ? n : 1); j0 += 32) {
           const int jc = BIG ? min(32, n - j0) : n;
@@ -955,7 +956,10 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           SFB_TSUB(7);
 
           // B': exact rows of the flagged partners (warp-uniform loop; shuffles need all lanes)  // @stage B_pair_exact
-          if (merge) pdef = mask;
+          if (merge && j0 + 32 >= (BIG ? n : 1)) {   // the last pair chunk joins the obstacle rows
+            pdef = mask;
+            pj0 = j0;
+          }
           else
           while (__any_sync(FULL, mask != 0u)) {
             const bool act = mask != 0u;
@@ -1056,7 +1060,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
             // TBL: a partner robot's exact positions come from the table (phase A), so each
             // lane runs its own rows without warp-synchronous exchanges; obstacle centres and
             // axes from shared memory (the pair axes are the double4 at sKD[KC_INV_A2])
-            while (TBL ? ((pmk | omk) != 0u) : __any_sync(FULL, (pmk | omk) != 0u)) {
+            // (n > 32: partner positions from the FP32 hi/lo rows, also per lane)
+            while ((TBL || BIG) ? ((pmk | omk) != 0u) : __any_sync(FULL, (pmk | omk) != 0u)) {
               const bool isp = pmk != 0u;
               const bool act = isp || omk != 0u;
               const int bit = __ffs(isp ? pmk : omk) - 1;          // -1: no row left
@@ -1072,6 +1077,18 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                   const int q1 = isp ? tb1 + ((a * n + jl) ^ sw1) : q0;
                   pj[a][0] = lds_f64(sbase + 8 * q0);
                   pj[a][1] = lds_f64(sbase + 8 * q1);
+                }
+              } else if (BIG) {
+                if (isp) {
+                  const float* hp = sPos + ((size_t)pslot * NROW + pj0 + jl) * ND2;
+                  const float* lp = sLo + ((size_t)pslot * NROW + pj0 + jl) * ND2;
+#pragma unroll
+                  for (int a = 0; a < ND; ++a)
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
+                } else {
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
                 }
               } else {
                 if (__any_sync(FULL, isp)) {
@@ -1095,7 +1112,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                 const double4 ax = *reinterpret_cast<const double4*>(isp ? sKD + KC_INV_A2 : sObsAx + 4 * o);
                 ia2 = ax.x; ib2 = ax.y; aa = ax.z; bb = ax.w;
               }
-              const bool once = !isp || i < jl;   // rows the reference's F holds once
+              const bool once = !isp || i < pj0 + jl;   // rows the reference's F holds once
               const double cs = once ? 1.0 : -1.0;
 #pragma unroll
               for (int kk = 0; kk < 2; ++kk) {
