@@ -598,7 +598,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     rbk = 0; wk = warp; nwk = nw;
   }
   const int i = BIG ? rbk * 32 + lane : lane % LW;
-  const bool robot_ok = keep<KEEP>(i < n ? 1 : 0) != 0;
+  const bool robot_ok = keep<KEEP || BIG>(i < n ? 1 : 0) != 0;
   const int ic = keep<KEEP>(robot_ok ? i : n - 1);
   const int NTS = (NKG + SUB - 1) / SUB;
   const int ts_lo = (NTS * crank) / csize, ts_hi = (NTS * (crank + 1)) / csize;
@@ -705,10 +705,10 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       SFB_JITTER(2, it * 64 + ts);
       const int pslot = BIG ? 2 * wk + (tcnt & 1) : 0;
       const int kg_raw = ts * SUB + sub;
-      const bool kg_ok = (!BIG && SUB == 1) || kg_raw < NKG;   // TBL: one k-group per task, ts < NTS = NKG
+      const bool kg_ok = SUB == 1 || kg_raw < NKG;   // one k-group per task: ts < NTS = NKG
       const int kg = kg_ok ? kg_raw : NKG - 1;
       const bool live = robot_ok && kg_ok;
-      const bool has1 = keep<KEEP>(2 * kg + 1 < K1 ? 1 : 0) != 0;
+      const bool has1 = keep<KEEP || BIG>(2 * kg + 1 < K1 ? 1 : 0) != 0;
       const double* w0r = sW + (size_t)(2 * kg) * WSTR;   // W rows of the two steps
       const double* w1r = w0r + WSTR;
 #ifdef SFB_PHASE_TIMING
