@@ -155,6 +155,22 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
   return v;
 }
 
+// exact FP64 positions (both steps) of a body from its FP32 hi / lo rows (16-B aligned,
+// (x0, x1, y0, y1[, z0, z1, 0, 0])): one vector load per row
+template <int ND>
+__device__ __forceinline__ void hilo_positions(const float* hp, const float* lp, double (&pj)[ND][2]) {
+  const float4 h = *reinterpret_cast<const float4*>(hp), l = *reinterpret_cast<const float4*>(lp);
+  pj[0][0] = (double)h.x + (double)l.x;
+  pj[0][1] = (double)h.y + (double)l.y;
+  pj[1][0] = (double)h.z + (double)l.z;
+  pj[1][1] = (double)h.w + (double)l.w;
+  if constexpr (ND == 3) {
+    const float2 h2 = *reinterpret_cast<const float2*>(hp + 4), l2 = *reinterpret_cast<const float2*>(lp + 4);
+    pj[ND - 1][0] = (double)h2.x + (double)l2.x;
+    pj[ND - 1][1] = (double)h2.y + (double)l2.y;
+  }
+}
+
 // append the sign bit of t (set = hit) below the bits already in m: (m << 1) | (t >> 31)
 __device__ __forceinline__ unsigned push_hit(unsigned m, unsigned t) { return __funnelshift_l(t, m, 1); }
 
@@ -970,11 +986,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
             if (BIG) {
               const float* hp = sPos + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
               const float* lp = sLo + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
-#pragma unroll
-              for (int a = 0; a < ND; ++a)
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk)
-                  pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
+              hilo_positions<ND>(hp, lp, pj);
             } else {
               const int src = sub * LW + jl;
 #pragma unroll
@@ -1082,10 +1094,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                 if (isp) {
                   const float* hp = sPos + ((size_t)pslot * NROW + pj0 + jl) * ND2;
                   const float* lp = sLo + ((size_t)pslot * NROW + pj0 + jl) * ND2;
-#pragma unroll
-                  for (int a = 0; a < ND; ++a)
-#pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) pj[a][kk] = (double)hp[2 * a + kk] + (double)lp[2 * a + kk];
+                  hilo_positions<ND>(hp, lp, pj);
                 } else {
 #pragma unroll
                   for (int a = 0; a < ND; ++a) pj[a][0] = pj[a][1] = sObsC[o * ND + a];
