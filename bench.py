@@ -477,7 +477,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        ref = CpuReference(L_cpu=args.cpu_iters if args.cpu_iters > 0 else 5, steps=2, warmup=1)
+        ref = CpuReference(L_cpu=args.cpu_iters if args.cpu_iters > 0 else 5, steps=3, warmup=2)
         try:
             vals = ref.run()
         finally:
