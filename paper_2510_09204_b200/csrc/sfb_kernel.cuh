@@ -378,7 +378,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // tensor-core contraction, instead of per-lane partials of G
   constexpr bool TBL = !BIG && NJ == 32;
   double* sTab = sGl;
-  const int TS = tab_stride(ND * n);
+  // column of (axis a, robot i) in the g table: a * 32 + i (32 columns per axis whatever n is, so
+  // the axis is an immediate offset and the swizzle only touches the robot index)
+  const int TS = tab_stride(ND * 32);
   // KKT scratch (aliases the union region (BIG) / the per-lane partials or g table after the
   // reduction; TBL rows it overwrites are rewritten by their task, or masked, before use)
   double* sD = reinterpret_cast<double*>(BIG ? uni : smem + P.L.gl);  // [ND*n][NXI]
@@ -660,7 +662,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     // g_i(k) once its rows are done (no other task reads them). Rows outside this CTA's steps
     // [klo, khi) are not stored (the contraction masks them).
     if (TBL) {
-      const int ncol = ND * n, ntn = (ncol + 7) >> 3;
+      const int ncol = ND * 32, ntn = ncol >> 3;         // table columns a * 32 + i
       const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
       const int mt0 = klo >> 3, ntm = ((khi + 7) >> 3) - mt0;
       const int rq = lane >> 2, kq = lane & 3;
@@ -675,11 +677,14 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       for (int item = warp; item < ntn * G; item += nw) {
         const int rg = item / ntn, nt2 = item - rg * ntn;
         const int colb = nt2 * 8 + rq, col = nt2 * 8 + 2 * kq;
+        // table column a * 32 + i <- xi row a * n + i (columns of robots i >= n: robot 0's values,
+        // never read by a task, and the contraction does not store them)
+        const int xrow_b = (colb >> 5) * n + ((colb & 31) < n ? (colb & 31) : 0);
         double bfr[NKS];
 #pragma unroll
         for (int ks = 0; ks < NKS; ++ks) {
           const int c = 4 * ks + kq;
-          bfr[ks] = (4 * NKS > NXP && c >= NXI) ? 0.0 : sXi[colb * NXP + c];   // crossed into the next row
+          bfr[ks] = (4 * NKS > NXP && c >= NXI) ? 0.0 : sXi[xrow_b * NXP + c];   // crossed into the next row
         }
         const bool pair_ok = col + 1 < ncol, one_ok = col < ncol;
         const double* wa = sW + ((mt0 + rg) * 8 + rq) * WSTR + kq;
@@ -742,8 +747,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #pragma unroll
       for (int a = 0; a < ND; ++a) {
         if (TBL) {
-          p[a][0] = tr0[(a * n + ic) ^ sw0];
-          p[a][1] = tr1[(a * n + ic) ^ sw1];
+          p[a][0] = tr0[a * 32 + (ic ^ sw0)];
+          p[a][1] = tr1[a * 32 + (ic ^ sw1)];
         } else {
           p[a][0] = p[a][1] = 0.0;
         }
@@ -1085,8 +1090,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                 // 32-bit shared-window addresses selected per row kind
 #pragma unroll
                 for (int a = 0; a < ND; ++a) {
-                  const int q0 = isp ? tb0 + ((a * n + jl) ^ sw0) : ob0 + o * ND + a;
-                  const int q1 = isp ? tb1 + ((a * n + jl) ^ sw1) : q0;
+                  const int q0 = isp ? tb0 + a * 32 + (jl ^ sw0) : ob0 + o * ND + a;
+                  const int q1 = isp ? tb1 + a * 32 + (jl ^ sw1) : q0;
                   pj[a][0] = lds_f64(sbase + 8 * q0);
                   pj[a][1] = lds_f64(sbase + 8 * q1);
                 }
@@ -1193,8 +1198,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           double* w1 = const_cast<double*>(tr1);
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
-            w0[(a * n + i) ^ sw0] = g[a][0];
-            if (has1) w1[(a * n + i) ^ sw1] = g[a][1];
+            w0[a * 32 + (i ^ sw0)] = g[a][0];
+            if (has1) w1[a * 32 + (i ^ sw1)] = g[a][1];
           }
         }
       } else if (__any_sync(FULL, nsteps > 0)) {
@@ -1300,7 +1305,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       // per 8-column tile, two 8-row tiles of c, k in steps of 4 over this CTA's steps [klo, khi)
       // (rows outside are masked, never read), even/odd k-steps in separate accumulators then
       // added: a fixed order, deterministic. A(m = c, k) = W[k][c], B(k, col) = g[k][col].
-      const int ncol = ND * n, ntl = (ncol + 7) >> 3;
+      const int ncol = ND * 32, ntl = ncol >> 3;         // table columns a * 32 + i
       const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
       const int rq = lane >> 2, kq = lane & 3;
       for (int tl = warp; tl < ntl; tl += nw) {
@@ -1359,7 +1364,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int col = tl * 8 + kq * 2 + j;
-            if (c < NXI && col < ncol) sG[col * NXI + c] = acc[0][mt][j] + acc[1][mt][j];
+            if (c < NXI && (col & 31) < n) sG[((col >> 5) * n + (col & 31)) * NXI + c] = acc[0][mt][j] + acc[1][mt][j];
           }
         }
       }
