@@ -604,6 +604,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   const float plim = fminf(P.plim * amin_all,
                            (float)(P.d_max * (1.0 - 1e-4) / (2.0 * sqrt((double)ND))) * amin_all);
   const double* opos = P.obs_pos + (size_t)inst * ND * m * K1;
+  // static obstacles in one chunk: the exact pair and obstacle rows run in one loop
+  const bool merge_rows = keep<KEEP || BIG>(P.obs_static && m > 0 && MP <= 32 ? 1 : 0) != 0;
 
   // lane -> (robot, k-group) mapping
   constexpr int LW = BIG ? 32 : NJ, SUB = 32 / LW;
@@ -901,7 +903,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
               q = __ffma2_rn(dx, dx, q);
               if ((int)(__float_as_uint(q.x) | __float_as_uint(q.y)) < 0) mm |= 1u << o;
             }
-            mm = __brev(mm << (32 - oc));   // undone by the shared bit reversal below
+            return live ? mm : 0u;   // bit o = obstacle o (one chunk: MP <= 32)
           } else if (P.obs_static) {
             // one row per obstacle: (-x, -y[, -z], -thr[, kappa]); packed ops broadcast the scalars
             const float* ob = sObsS + (size_t)o0 * OS;
@@ -956,7 +958,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
         // n <= 32 with static obstacles (one chunk): the exact pair and obstacle rows run in one
         // loop, a lane's pair bits first then its obstacle bits — each lane's order of the
         // two-loop form, in max(pairs + obstacles) instead of max(pairs) + max(obstacles) steps
-        const bool merge = P.obs_static && m > 0 && MP <= 32;
+        const bool merge = merge_rows;
         unsigned pdef = 0u;
         int pj0 = 0;   // first robot of the pair chunk deferred to the merged loop
         // B: robots, in chunks of 32 bodies (one chunk of NJ for n <= 32)
@@ -1089,9 +1091,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
               if (TBL) {
                 // 32-bit shared-window addresses selected per row kind
 #pragma unroll
-                for (int a = 0; a < ND; ++a) {
-                  const int q0 = isp ? tb0 + a * 32 + (jl ^ sw0) : ob0 + o * ND + a;
-                  const int q1 = isp ? tb1 + a * 32 + (jl ^ sw1) : q0;
+                for (int a = 0; a < ND; ++a) {   // (in this per-lane loop bit >= 0)
+                  const int q0 = isp ? tb0 + a * 32 + (bit ^ sw0) : ob0 + bit * ND + a;
+                  const int q1 = isp ? tb1 + a * 32 + (bit ^ sw1) : q0;
                   pj[a][0] = lds_f64(sbase + 8 * q0);
                   pj[a][1] = lds_f64(sbase + 8 * q1);
                 }
@@ -1119,14 +1121,14 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
               }
               double ia2, ib2, aa, bb;
               if (TBL) {
-                const uint32_t axa = sbase + (isp ? P.L.kc + KC_INV_A2 * 8 : P.L.obs_ax + 32 * o);
+                const uint32_t axa = sbase + (isp ? P.L.kc + KC_INV_A2 * 8 : P.L.obs_ax + 32 * bit);
                 const double2 a01 = lds_f64x2(axa), a23 = lds_f64x2(axa + 16);
                 ia2 = a01.x; ib2 = a01.y; aa = a23.x; bb = a23.y;
               } else {
                 const double4 ax = *reinterpret_cast<const double4*>(isp ? sKD + KC_INV_A2 : sObsAx + 4 * o);
                 ia2 = ax.x; ib2 = ax.y; aa = ax.z; bb = ax.w;
               }
-              const bool once = !isp || i < pj0 + jl;   // rows the reference's F holds once
+              const bool once = !isp || i < pj0 + (TBL ? bit : jl);   // rows the reference's F holds once
               const double cs = once ? 1.0 : -1.0;
 #pragma unroll
               for (int kk = 0; kk < 2; ++kk) {
