@@ -823,6 +823,24 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       const float2 ny = make_float2(-own[1][0], -own[1][1]);
       const float2 nz = (ND == 3) ? make_float2(-own[ND - 1][0], -own[ND - 1][1]) : make_float2(0.f, 0.f);
       const int nsteps = live ? (has1 ? 2 : 1) : 0;
+      // obstacle-grid candidates of the lane's two positions, looked up before the pair screen
+      // so the shared-memory latency overlaps it (the FMA's rounding moves a cell coordinate by
+      // ~1e-5 of a cell, well inside the cells' 1e-3 widening)
+      // (n <= 32 only: the n > 32 builds have no register to keep it across the pair chunks)
+      auto grid_lookup = [&]() -> unsigned {
+        if (!live) return 0u;
+        const float4 gk = *reinterpret_cast<const float4*>(sKF + KC_F_GX0);   // bx by ax ay
+        const float2 ux = __ffma2_rn(make_float2(own[0][0], own[0][1]), make_float2(gk.z, gk.z), make_float2(gk.x, gk.x));
+        const float2 uy = __ffma2_rn(make_float2(own[1][0], own[1][1]), make_float2(gk.w, gk.w), make_float2(gk.y, gk.y));
+        auto cell = [&](float u, float v) -> unsigned {
+          const int cx = __float2int_rd(u), cy = __float2int_rd(v);
+          return ((unsigned)(cx | cy) < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
+        };
+        unsigned c = cell(ux.x, uy.x);
+        if (has1) c |= cell(ux.y, uy.y);
+        return c;
+      };
+      const unsigned grid_cand = (TBL && compact && !force) ? grid_lookup() : 0u;
       SFB_TSUB(6);
 
       double g[ND][2];  // @stage B_pair_screen
@@ -874,16 +892,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           if (compact) {
             // grid candidates of the lane's two positions, each confirmed by the FP32 test
             // (per lane: a robot is near few obstacles)
-            // (the FMA's rounding moves u by ~1e-5 of a cell, well inside the cells' 1e-3 widening)
-            const float4 gk = *reinterpret_cast<const float4*>(sKF + KC_F_GX0);   // bx by ax ay
-            const float2 ux = __ffma2_rn(make_float2(own[0][0], own[0][1]), make_float2(gk.z, gk.z), make_float2(gk.x, gk.x));
-            const float2 uy = __ffma2_rn(make_float2(own[1][0], own[1][1]), make_float2(gk.w, gk.w), make_float2(gk.y, gk.y));
-            auto cell = [&](float u, float v) -> unsigned {
-              const int cx = __float2int_rd(u), cy = __float2int_rd(v);
-              return ((unsigned)(cx | cy) < (unsigned)GRID) ? sGrid[cy * GRID + cx] : 0u;
-            };
-            unsigned cand = live ? cell(ux.x, uy.x) : 0u;
-            if (live && has1) cand |= cell(ux.y, uy.y);
+            // (cells looked up before the pair screen: grid_cand)
+            unsigned cand = o0 != 0 ? 0u : (TBL ? grid_cand : grid_lookup());
             while (cand) {
               const int o = __ffs(cand) - 1;
               cand &= cand - 1u;
