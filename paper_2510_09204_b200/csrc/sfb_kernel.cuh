@@ -362,7 +362,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   float* sObsS = reinterpret_cast<float*>(smem + P.L.obs_s);       // [MP][OS] static: -x -y (-z) -thr (kappa)
   float* sObs = reinterpret_cast<float*>(smem + P.L.obs);          // [NKG][MP][ND2] (dynamic)
   float* sPmax = reinterpret_cast<float*>(smem + P.L.pmax);        // [kgs][8] (n > 32)
-  unsigned char* uni = smem + P.L.uni;
+  unsigned char* uni = smem + keep<BIG>(P.L.uni);
   const int NROW = BIG ? n : NJ;                                    // bodies per k-group row
   // n > 32: positions of every k-group are shared by the robot-block warps of that k-group;
   // n <= 32: a warp holds all robots of its k-groups, so it owns a private position row
@@ -617,7 +617,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     sub = lane / LW;
     rbk = 0; wk = warp; nwk = nw;
   }
-  const int i = BIG ? rbk * 32 + lane : lane % LW;
+  const int i = BIG ? keep<BIG>(rbk * 32 + lane) : lane % LW;
   const bool robot_ok = keep<KEEP || BIG>(i < n ? 1 : 0) != 0;
   const int ic = keep<KEEP>(robot_ok ? i : n - 1);
   const int NTS = (NKG + SUB - 1) / SUB;
