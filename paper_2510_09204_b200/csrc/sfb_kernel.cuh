@@ -313,7 +313,7 @@ __host__ __device__ constexpr bool split_build() { return ND == 2 && !BIG2; }
 // PIECE_HEAD the loop stops before evaluation `stop` (read from shared memory each iteration,
 // so no register holds it across the solve) and hands the state to slot blockIdx.x.
 // Returns true when the member finished (converged or reached max_iters), outputs written.
-template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW>
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW, bool TW = false>
 __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const int piece,
                                           const int stop) {  // @stage setup
   constexpr int ND2 = (ND == 2) ? 4 : 8;   // floats per body per k-group
@@ -377,10 +377,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // (row stride TS, XOR-swizzled columns: conflict-free DMMA fragment loads) for the
   // tensor-core contraction, instead of per-lane partials of G
   constexpr bool TBL = !BIG && NJ == 32;
+  // TW (the 16-warp n = 33..64 build when its table fits): the same table-based positions
+  // (phase A) and DMMA contraction as TBL, with robot blocks of 32 as tasks
+  static_assert(!TW || (BIG && BIG2 && MW == 16 && ND == 2), "table build: 16-warp n = 33..64, 2D");
+  constexpr bool TAB = TBL || TW;
+  constexpr int CA = TW ? 64 : 32;   // table columns per axis
   double* sTab = sGl;
-  // column of (axis a, robot i) in the g table: a * 32 + i (32 columns per axis whatever n is, so
+  // column of (axis a, robot i) in the g table: a * CA + i (CA columns per axis whatever n is, so
   // the axis is an immediate offset and the swizzle only touches the robot index)
-  const int TS = tab_stride(ND * 32);
+  const int TS = tab_stride(ND * CA);
   // KKT scratch (aliases the union region (BIG) / the per-lane partials or g table after the
   // reduction; TBL rows it overwrites are rewritten by their task, or masked, before use)
   double* sD = reinterpret_cast<double*>(BIG ? uni : smem + P.L.gl);  // [ND*n][NXI]
@@ -412,7 +417,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     const int k = idx / WSTR, c = idx - k * WSTR;
     sW[idx] = (k < K1 && c < NXI) ? P.consts[co.W + k * NXI + c] : 0.0;
   }
-  if (TBL) {   // g-table rows K1 .. (K1 rounded up to 4) are read by the contraction, never written
+  if (TAB) {   // g-table rows K1 .. (K1 rounded up to 4) are read by the contraction, never written
     for (int idx = tid; idx < (((K1 + 3) & ~3) - K1) * TS; idx += nt) sTab[(size_t)K1 * TS + idx] = 0.0;
   }
   for (int idx = tid; idx < NB * NXI; idx += nt) sE[idx] = P.consts[co.E + idx];
@@ -663,8 +668,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     // task reads its own and its partners' positions from there and overwrites its rows with
     // g_i(k) once its rows are done (no other task reads them). Rows outside this CTA's steps
     // [klo, khi) are not stored (the contraction masks them).
-    if (TBL) {
-      const int ncol = ND * 32, ntn = ncol >> 3;         // table columns a * 32 + i
+    if (TAB) {
+      const int ncol = ND * CA, ntn = ncol >> 3;         // table columns a * CA + i
       const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
       const int mt0 = klo >> 3, ntm = ((khi + 7) >> 3) - mt0;
       const int rq = lane >> 2, kq = lane & 3;
@@ -679,9 +684,9 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       for (int item = warp; item < ntn * G; item += nw) {
         const int rg = item / ntn, nt2 = item - rg * ntn;
         const int colb = nt2 * 8 + rq, col = nt2 * 8 + 2 * kq;
-        // table column a * 32 + i <- xi row a * n + i (columns of robots i >= n: robot 0's values,
+        // table column a * CA + i <- xi row a * n + i (columns of robots i >= n: robot 0's values,
         // never read by a task, and the contraction does not store them)
-        const int xrow_b = (colb >> 5) * n + ((colb & 31) < n ? (colb & 31) : 0);
+        const int xrow_b = (colb / CA) * n + ((colb & (CA - 1)) < n ? (colb & (CA - 1)) : 0);
         double bfr[NKS];
 #pragma unroll
         for (int ks = 0; ks < NKS; ++ks) {
@@ -711,7 +716,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     constexpr int RA = BIG ? ND : (SFB_GREG > ND ? ND : SFB_GREG);
     double Gp[RA > 0 ? RA : 1][NXI];
     double* gl = sGl + (size_t)warp * NXI * ND * 32 + lane;          // this lane's partials, stride 32
-    if (!TBL) {
+    if (!TAB) {
 #pragma unroll
       for (int a = 0; a < ND; ++a)
 #pragma unroll
@@ -748,15 +753,15 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       double p[ND][2];
 #pragma unroll
       for (int a = 0; a < ND; ++a) {
-        if (TBL) {
-          p[a][0] = tr0[a * 32 + (ic ^ sw0)];
-          p[a][1] = tr1[a * 32 + (ic ^ sw1)];
+        if (TAB) {
+          p[a][0] = tr0[a * CA + (ic ^ sw0)];
+          p[a][1] = tr1[a * CA + (ic ^ sw1)];
         } else {
           p[a][0] = p[a][1] = 0.0;
         }
       }
 #pragma unroll
-      for (int c = 0; !TBL && c + 1 < NXI; c += 2) {
+      for (int c = 0; !TAB && c + 1 < NXI; c += 2) {
         const double2 u0 = *reinterpret_cast<const double2*>(w0r + c);
         const double2 u1 = *reinterpret_cast<const double2*>(w1r + c);
 #pragma unroll
@@ -766,7 +771,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           p[a][1] = fma(u1.y, x.y, fma(u1.x, x.x, p[a][1]));
         }
       }
-      if (!TBL && (NXI & 1)) {
+      if (!TAB && (NXI & 1)) {
         const double u0 = w0r[NXI - 1], u1 = w1r[NXI - 1];
 #pragma unroll
         for (int a = 0; a < ND; ++a) {
@@ -794,7 +799,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
           float4* dst = reinterpret_cast<float4*>(BIG ? sPos + ((size_t)pslot * NROW + i) * ND2 : posw + i * ND2);
           dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           if (ND == 3) dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-          if (BIG) {
+          if (BIG && !TW) {   // (TW: exact partner positions come from the table)
             float lv[ND2];
 #pragma unroll
             for (int a = 0; a < ND; ++a) {
@@ -1000,7 +1005,14 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
             mask &= mask - 1u;
             const int j = j0 + jl;
             double pj[ND][2];
-            if (BIG) {
+            if (TW) {
+              const int jj = act ? j : 0;
+#pragma unroll
+              for (int a = 0; a < ND; ++a) {
+                pj[a][0] = tr0[a * CA + (jj ^ sw0)];
+                pj[a][1] = tr1[a * CA + (jj ^ sw1)];
+              }
+            } else if (BIG) {
               const float* hp = sPos + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
               const float* lp = sLo + ((size_t)pslot * NROW + (act ? j : 0)) * ND2;
               hilo_positions<ND>(hp, lp, pj);
@@ -1108,7 +1120,13 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                   pj[a][1] = lds_f64(sbase + 8 * q1);
                 }
               } else if (BIG) {
-                if (isp) {
+                if (isp && TW) {
+#pragma unroll
+                  for (int a = 0; a < ND; ++a) {
+                    pj[a][0] = tr0[a * CA + ((pj0 + jl) ^ sw0)];
+                    pj[a][1] = tr1[a * CA + ((pj0 + jl) ^ sw1)];
+                  }
+                } else if (isp) {
                   const float* hp = sPos + ((size_t)pslot * NROW + pj0 + jl) * ND2;
                   const float* lp = sLo + ((size_t)pslot * NROW + pj0 + jl) * ND2;
                   hilo_positions<ND>(hp, lp, pj);
@@ -1203,15 +1221,18 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 
       // C: TBL stores g_i(k) for the tensor-core contraction after the task loop; otherwise
       // contraction with W^T into the lane's partial G  // @stage C_contract
-      if (TBL) {
-        __syncwarp();   // every lane's rows have read the partner positions of these steps
+      if (TAB) {
+        // every lane's rows have read the partner positions of these steps (TW: the rows of the
+        // k-group's other robot blocks too)
+        if (TW) asm volatile("bar.sync %0, %1;" ::"r"(1 + wk), "r"(P.RB * 32) : "memory");
+        else __syncwarp();
         if (live) {
           double* w0 = const_cast<double*>(tr0);
           double* w1 = const_cast<double*>(tr1);
 #pragma unroll
           for (int a = 0; a < ND; ++a) {
-            w0[a * 32 + (i ^ sw0)] = g[a][0];
-            if (has1) w1[a * 32 + (i ^ sw1)] = g[a][1];
+            w0[a * CA + (i ^ sw0)] = g[a][0];
+            if (has1) w1[a * CA + (i ^ sw1)] = g[a][1];
           }
         }
       } else if (__any_sync(FULL, nsteps > 0)) {
@@ -1312,12 +1333,12 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     if (tid == 0) t_sub = clock64();
 #endif
 
-    if (TBL) {
+    if (TAB) {
       // G^T (c x col) = W^T (c x k) . g (k x col) on the FP64 tensor cores (DMMA m8n8k4): warp
       // per 8-column tile, two 8-row tiles of c, k in steps of 4 over this CTA's steps [klo, khi)
       // (rows outside are masked, never read), even/odd k-steps in separate accumulators then
       // added: a fixed order, deterministic. A(m = c, k) = W[k][c], B(k, col) = g[k][col].
-      const int ncol = ND * 32, ntl = ncol >> 3;         // table columns a * 32 + i
+      const int ncol = ND * CA, ntl = ncol >> 3;         // table columns a * CA + i
       const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
       const int rq = lane >> 2, kq = lane & 3;
       for (int tl = warp; tl < ntl; tl += nw) {
@@ -1376,7 +1397,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int col = tl * 8 + kq * 2 + j;
-            if (c < NXI && (col & 31) < n) sG[((col >> 5) * n + (col & 31)) * NXI + c] = acc[0][mt][j] + acc[1][mt][j];
+            if (c < NXI && (col & (CA - 1)) < n) sG[((col / CA) * n + (col & (CA - 1))) * NXI + c] = acc[0][mt][j] + acc[1][mt][j];
           }
         }
       }
@@ -1404,7 +1425,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     }
     // n > 32: G partials in slots; slot s of round r holds warp r*slots + s, layout [ND][32][NXI]
     const int slots = P.L.slots;
-    for (int w0 = 0; BIG && w0 < nw; w0 += slots) {
+    for (int w0 = 0; BIG && !TW && w0 < nw; w0 += slots) {
       if (warp >= w0 && warp < w0 + slots && robot_ok) {
         double* dst = sSlot + (size_t)(warp - w0) * ND * 32 * NXI;
 #pragma unroll
@@ -1780,7 +1801,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 
 // MW = 16: the capped n > 32 build with 16-warp CTAs, one per SM (small batches and n = 65..128,
 // whose layout does not fit half an SM)
-template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW>
+template <int ND, int NXI, int NJ, bool BIG, bool BIG2 = false, int MW = NW, bool TW = false>
 __global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) : SFB_MINB)
     sf_solve_kernel(const KParams P) {
   // Split schedule ("stream-K" over evaluation units): with B > G resident CTAs, one CTA per
@@ -1801,7 +1822,7 @@ __global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) 
   if (!split_build<ND, BIG, BIG2>() || !P.split) {
     if (threadIdx.x == 0) sched[SCHED_MEMBER] = blockIdx.x / P.csize;
     __syncthreads();
-    sf_member<ND, NXI, NJ, BIG, BIG2, MW>(P, 0, PIECE_WHOLE, 0);
+    sf_member<ND, NXI, NJ, BIG, BIG2, MW, TW>(P, 0, PIECE_WHOLE, 0);
     return;
   }
   if (threadIdx.x == 0) sched[SCHED_PIECE] = 0u;
@@ -1841,7 +1862,7 @@ __global__ void __launch_bounds__(MW * 32, BIG ? (BIG2 ? (MW > NW ? 1 : 2) : 1) 
     }
     if (threadIdx.x == 0) sched[SCHED_MEMBER] = b;
     __syncthreads();
-    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2, MW>(P, it0, piece, stop);
+    const bool fin = sf_member<ND, NXI, NJ, BIG, BIG2, MW, TW>(P, it0, piece, stop);
     __syncthreads();                              // shared memory reused by the next piece; handoff stores issued
     if (threadIdx.x == 0) {
       const int pcn = (int)sched[SCHED_PIECE];
