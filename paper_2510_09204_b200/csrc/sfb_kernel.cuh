@@ -376,12 +376,12 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // TBL (one k-group row of 32 robots per warp task): g_i(k) goes to a [k][axis * n + i] table
   // (row stride TS, XOR-swizzled columns: conflict-free DMMA fragment loads) for the
   // tensor-core contraction, instead of per-lane partials of G
-  constexpr bool TBL = !BIG && NJ == 32;
+  constexpr bool TBL = !BIG && (NJ == 32 || NJ == 16);   // (n = 9..16: two k-groups per warp task)
   // TW (the 16-warp n = 33..64 build when its table fits): the same table-based positions
   // (phase A) and DMMA contraction as TBL, with robot blocks of 32 as tasks
   static_assert(!TW || (BIG && BIG2 && MW == 16 && ND == 2), "table build: 16-warp n = 33..64, 2D");
   constexpr bool TAB = TBL || TW;
-  constexpr int CA = TW ? 64 : 32;   // table columns per axis
+  constexpr int CA = TW ? 64 : NJ;   // table columns per axis
   double* sTab = sGl;
   // column of (axis a, robot i) in the g table: a * CA + i (CA columns per axis whatever n is, so
   // the axis is an immediate offset and the swizzle only touches the robot index)
@@ -670,7 +670,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
     // [klo, khi) are not stored (the contraction masks them).
     if (TAB) {
       const int ncol = ND * CA, ntn = ncol >> 3;         // table columns a * CA + i
-      const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
+      const int klo = 2 * SUB * ts_lo, khi = min(K1, 2 * SUB * ts_hi);
       const int mt0 = klo >> 3, ntm = ((khi + 7) >> 3) - mt0;
       const int rq = lane >> 2, kq = lane & 3;
       constexpr int NKS = (NXI + 3) / 4;
@@ -1114,8 +1114,8 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
                 // 32-bit shared-window addresses selected per row kind
 #pragma unroll
                 for (int a = 0; a < ND; ++a) {   // (in this per-lane loop bit >= 0)
-                  const int q0 = isp ? tb0 + a * 32 + (bit ^ sw0) : ob0 + bit * ND + a;
-                  const int q1 = isp ? tb1 + a * 32 + (bit ^ sw1) : q0;
+                  const int q0 = isp ? tb0 + a * CA + (bit ^ sw0) : ob0 + bit * ND + a;
+                  const int q1 = isp ? tb1 + a * CA + (bit ^ sw1) : q0;
                   pj[a][0] = lds_f64(sbase + 8 * q0);
                   pj[a][1] = lds_f64(sbase + 8 * q1);
                 }
@@ -1339,7 +1339,7 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
       // (rows outside are masked, never read), even/odd k-steps in separate accumulators then
       // added: a fixed order, deterministic. A(m = c, k) = W[k][c], B(k, col) = g[k][col].
       const int ncol = ND * CA, ntl = ncol >> 3;         // table columns a * CA + i
-      const int klo = 2 * ts_lo, khi = min(K1, 2 * ts_hi);
+      const int klo = 2 * SUB * ts_lo, khi = min(K1, 2 * SUB * ts_hi);
       const int rq = lane >> 2, kq = lane & 3;
       for (int tl = warp; tl < ntl; tl += nw) {
         double acc[2][2][2];   // [parity][m tile][2]
