@@ -376,12 +376,12 @@ __device__ __forceinline__ bool sf_member(const KParams& P, const int it0, const
   // TBL (one k-group row of 32 robots per warp task): g_i(k) goes to a [k][axis * n + i] table
   // (row stride TS, XOR-swizzled columns: conflict-free DMMA fragment loads) for the
   // tensor-core contraction, instead of per-lane partials of G
-  constexpr bool TBL = !BIG && (NJ == 32 || NJ == 16);   // (n = 9..16: two k-groups per warp task)
+  constexpr bool TBL = !BIG;   // (n <= 16: 32 / NJ k-groups per warp task)
   // TW (the 16-warp n = 33..64 build when its table fits): the same table-based positions
   // (phase A) and DMMA contraction as TBL, with robot blocks of 32 as tasks
   static_assert(!TW || (BIG && BIG2 && MW == 16 && ND == 2), "table build: 16-warp n = 33..64, 2D");
   constexpr bool TAB = TBL || TW;
-  constexpr int CA = TW ? 64 : NJ;   // table columns per axis
+  constexpr int CA = TW ? 64 : (NJ < 16 ? 16 : NJ);   // table columns per axis (>= 16: the swizzle stays in range)
   double* sTab = sGl;
   // column of (axis a, robot i) in the g table: a * CA + i (CA columns per axis whatever n is, so
   // the axis is an immediate offset and the swizzle only touches the robot index)
